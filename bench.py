@@ -1,0 +1,318 @@
+"""Benchmark: binary64 exp HR search, args tested/sec (BASELINE.json metric).
+
+Workload (BASELINE.json configs[2]): exp over binade [1,2)
+of binary64, 2^40 consecutive arguments per GPU (weak scaling: rank r owns
+indices [r 2^40, (r+1) 2^40)), domains of N = 2^15 arguments, super-domains
+of 2^24 arguments (tau = 512 Taylor blocks, delta = 2, F = 96, L = 8),
+eps = 2^-32, regular search, phase-2 split 8.  One step = the whole device
+hot path over the slice (tabulated walk + Boolean tests + search +
+compaction, phase 2, phase 3, ordered candidate output): hrb_run_slice.
+The host Taylor generation (mpmath, reused unchanged from the paper's
+hybrid split) runs once before timing; its rate is reported separately.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+Prints one JSON line on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "binary64 args tested/sec (exp) at 1/2/4/8 B200 vs CPU ref; % of INT-pipe peak"
+UNIT = "args/s"
+KERNELS_PER_STEP = 16  # prep, 2 scan, phase1, 3 compact, phase2, 3 compact, phase3, 3 scan, scatter
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--log2-args", type=int, default=40)
+    ap.add_argument("--eps-bits", type=int, default=32)
+    ap.add_argument("--algo", default="regular", choices=("regular", "lefevre"))
+    ap.add_argument("--log2-super", type=int, default=24)
+    ap.add_argument("--log2-N", type=int, default=15)
+    ap.add_argument("--cpu-sample-log2", type=int, default=36, help="arguments in the CPU-baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def make_cfg(args):
+    from paper_1211_3056_b200 import FpFormat, PhaseConfig, PipelineConfig, PolyGenConfig
+
+    N = 1 << args.log2_N
+    tau = 1 << (args.log2_super - args.log2_N)
+    mu = 1 << ((args.log2_super - args.log2_N) // 2)
+    pg = PolyGenConfig(tau=tau, N=N, mu=mu, nu=tau // mu, delta=2, limbs=8, frac_bits=96, guard=32)
+    return PipelineConfig("exp", FpFormat(53, args.eps_bits), pg, PhaseConfig(args.algo, phase2_split=8, N1=N))
+
+
+def prepare(args, start, count, workers):
+    from paper_1211_3056_b200.funnel import prepare_slice
+
+    t0 = time.perf_counter()
+    batch = prepare_slice("exp", 0, start, count, make_cfg(args), workers=workers)
+    return batch, time.perf_counter() - t0
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                vals = [v.strip() for v in out.stdout.strip().split(",")]
+                if len(vals) == 6:
+                    self.samples.append(vals)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({names[k] for s in self.samples for k in range(4) if s[2 + k].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def load_calibration():
+    p = os.path.join(ROOT, "profiles", "calibration.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            return json.load(fh)
+    return {}
+
+
+def cpu_baseline(args, sample_log2: int):
+    """The oracle port (oracle/hr_oracle.c, OpenMP over all host threads)
+    timed on a bounded contiguous sample of the same workload."""
+    import oracle
+
+    oracle.build()
+    count = 1 << sample_log2
+    batch, _ = prepare(args, 0, count, os.cpu_count() or 1)
+    threads = oracle.threads()
+    t0 = time.perf_counter()
+    fails = oracle.phase1(batch, args.algo, 1)
+    rows = oracle.phase2(batch, args.algo, 1, 8, fails)
+    oracle.phase3(batch, rows)
+    dt = time.perf_counter() - t0
+    return {"value": count / dt, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"exp p=53 indices [0, 2^{sample_log2}) (same config), phases 1-3, {dt:.2f} s"}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import oracle
+
+    oracle.build()
+    count = 1 << args.cpu_sample_log2
+    batch, _ = prepare(args, 0, count, os.cpu_count() or 1)
+    times = []
+    for k in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        fails = oracle.phase1(batch, args.algo, 1)
+        rows = oracle.phase2(batch, args.algo, 1, 8, fails)
+        oracle.phase3(batch, rows)
+        if k >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    v = count / float(np.mean(times))
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(times)),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic: exp binade [1,2) argument range (real Taylor blocks)",
+            "config": {"workload": f"exp p=53 eps=2^-{args.eps_bits} N=2^{args.log2_N} CPU sample 2^{args.cpu_sample_log2} "
+                                   f"args (of the 2^{args.log2_args}/GPU slice)", "algo": args.algo},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": oracle.threads(), "kind": "port",
+                             "sample": f"indices [0, 2^{args.cpu_sample_log2}), phases 1-3 per step"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    rank, world, local = dist_env()
+    import torch
+
+    from paper_1211_3056_b200.device import DeviceSlice, FusedRunner, run_host
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    count = 1 << args.log2_args
+    workers = max(1, (os.cpu_count() or 1) // max(1, int(os.environ.get("LOCAL_WORLD_SIZE", world))))
+    batch, prep_s = prepare(args, rank * count, count, workers)
+    algo = 2 if args.algo == "regular" else 0
+    ds = DeviceSlice(batch)
+    sub_cap = max(1 << 16, batch.n_total * 2)
+    runner = FusedRunner(ds, algo, 1, 8, sub_cap=sub_cap, cand_cap=1 << 20)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        runner.launch()
+    torch.cuda.synchronize()
+    counts0 = runner.counts_host().copy()
+    # phase-1 kernel alone, for the roofline (same stream, CUDA events)
+    from paper_1211_3056_b200 import _native as nat
+    import ctypes as C
+
+    lib = nat.load()
+    p1_ms = []
+    cnt = ds.empty64(4)
+    for _ in range(max(3, args.steps // 2)):
+        cnt.zero_()
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        nat.check("hrb_phase1", lib.hrb_phase1(C.byref(ds.desc), algo, 1, runner.fail.data_ptr(), cnt.data_ptr(),
+                                               batch.n_total, cnt[3:].data_ptr(), nat.stream_ptr()))
+        e1.record(stream)
+        torch.cuda.synchronize()
+        p1_ms.append(e0.elapsed_time(e1))
+    iters = int(cnt.cpu().numpy().view(np.uint64)[3])
+    # timed region
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    sampler = ClockSampler(local)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with sampler:
+        for k in range(args.steps):
+            flush.zero_()
+            evs[k][0].record(stream)
+            runner.launch()
+            evs[k][1].record(stream)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    ms = float(np.mean(step_ms))
+    counts = runner.counts_host().copy()
+    assert np.array_equal(counts, counts0), "non-deterministic counts across steps"
+    # e2e: the C-ABI host-buffer entry point (H2D of the packed slice, all
+    # kernels, D2H of counts + failing ids + candidates), wall clock
+    e2e = None
+    if not args.no_e2e:
+        pinned = {}
+        for name in ("coef", "G", "s2abs", "n_dom", "dom_n", "last_n", "dom_base", "m0"):
+            arr = getattr(batch, name)
+            t = torch.from_numpy(arr.view(np.int32 if arr.dtype == np.uint32 else np.int64)).pin_memory()
+            pinned[name] = t
+            setattr(batch, name, t.numpy().view(arr.dtype))
+        run_host(batch, algo, 1, 8)
+        e2e_t = []
+        for _ in range(max(2, args.steps // 2)):
+            t0 = time.perf_counter()
+            hc, hf, hm, hd, hdom, _ = run_host(batch, algo, 1, 8)
+            e2e_t.append(time.perf_counter() - t0)
+        e2e_ms = 1e3 * float(np.mean(e2e_t))
+        h2d = batch.nbytes()
+        d2h = 32 + 8 * int(hc[0]) + 24 * int(hc[2])
+        e2e = {"value": count * world / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms}
+    # max over ranks
+    t_all = torch.tensor([ms, float(np.mean(p1_ms))], device="cuda")
+    if dist:
+        dist.all_reduce(t_all, op=dist.ReduceOp.MAX)
+        allc = torch.tensor(counts.astype(np.int64), device="cuda")
+        dist.all_reduce(allc)  # end-of-run gather of the per-rank counters (NCCL)
+        tot_counts = allc.cpu().numpy()
+    else:
+        tot_counts = counts.astype(np.int64)
+    ms_max, p1_max = float(t_all[0]), float(t_all[1])
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+    value = count * world / (ms_max / 1e3)
+    clocks = sampler.summary()
+    calib = load_calibration()
+    instr_per_step = calib.get("phase1_int_lane_instr_per_step")
+    sm_mhz = clocks.get("sm_mhz") or 1965.0
+    peak_tops = 148 * 128 * sm_mhz * 1e6 / 1e12  # alu + fma pipes: 1 warp-instr/clk/SMSP
+    achieved = (iters * instr_per_step / (p1_max / 1e3) / 1e12) if instr_per_step else None
+    roofline = {"bound": "int", "kernel": "phase1_kernel", "unit": "Tops/s",
+                "achieved": achieved, "peak": peak_tops,
+                "peak_basis": "148 SM x 128 INT lanes/clk (alu+fma pipes) x median SM clock under load",
+                "frac": (achieved / peak_tops) if achieved else None,
+                "traffic": calib.get("phase1_dram_bytes_per_launch"),
+                "quotient_steps_per_launch": iters, "phase1_ms": p1_max,
+                "steps_per_s": iters / (p1_max / 1e3),
+                "int_lane_instr_per_step": instr_per_step}
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic: exp binade [1,2) argument ranges, Taylor blocks generated on the host (mpmath)",
+            "config": {"workload": f"exp p=53 2^{args.log2_args} args/GPU eps=2^-{args.eps_bits} "
+                                   f"N=2^{args.log2_N} super=2^{args.log2_super} delta=2 F=96 split=8 {args.algo}",
+                       "parallelism": f"shard{world} (contiguous argument blocks, no collective on the hot path)",
+                       "l2": "flushed between steps (256 MiB write)",
+                       "domains_per_gpu": batch.n_total, "phase1_fail": int(tot_counts[0]),
+                       "phase2_survivors": int(tot_counts[1]), "candidates": int(tot_counts[2])},
+            "clocks": clocks, "gpu_launches": KERNELS_PER_STEP * args.steps, "roofline": roofline,
+            "host_polygen": {"seconds": prep_s, "workers": workers, "super_domains": batch.n_super,
+                             "args_per_s": count / prep_s},
+            "e2e": e2e}
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args, args.cpu_sample_log2)
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

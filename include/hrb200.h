@@ -1,0 +1,176 @@
+/*
+ * hrb200.h -- C-ABI of the B200-native hard-to-round (HR) case search.
+ *
+ * This is the drop-in boundary between the host (Python `hardround`-shaped
+ * package, polynomial generation, error bounds, confirmation) and the
+ * sm_100a kernels.  Every function is extern "C", takes plain pointers and
+ * sizes, returns an int status and never throws.  Unless stated otherwise
+ * pointers are DEVICE pointers owned by the caller and work is enqueued on
+ * the caller's cudaStream_t (passed as void*; NULL = legacy default stream).
+ *
+ * Each entry point names the reference interface it replaces
+ * (/root/reference/pkg/src/hardround/<file>:<line>).
+ */
+#ifndef HRB200_H
+#define HRB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes --------------------------------------------------- */
+#define HRB_OK 0           /* success                                        */
+#define HRB_ERR_RUNTIME 1  /* CUDA error (cli.py:268 exit 1 analogue)         */
+#define HRB_ERR_CONFIG 2   /* invalid argument (ValueError, cli.py:264-266)  */
+#define HRB_ERR_OVERFLOW 4 /* reserved: limb overflow (MPOverflowError)      */
+#define HRB_ERR_CAPACITY 8 /* an output buffer was too small; counts are the
+                              true totals so the caller can re-run larger   */
+
+/* ---- enums (values fixed: they cross the ABI) ----------------------- */
+/* lowerbound.py:41-45 Algorithm */
+#define HRB_ALGO_LEFEVRE 0
+#define HRB_ALGO_LEFEVRE_SWAP 1
+#define HRB_ALGO_REGULAR 2
+#define HRB_ALGO_REGULAR_UNROLLED 3
+/* lowerbound.py:80-85 _mode_code (fixedpoint.py:26-33 DivisionMode) */
+#define HRB_MODE_SUBTRACTIVE 0
+#define HRB_MODE_HYBRID 1
+#define HRB_MODE_HARDWARE 2
+
+int hrb_version(void);                  /* 100*major + minor                 */
+const char* hrb_last_error(void);       /* thread-local message of last error */
+int hrb_device_info(int device, char* buf, int buflen); /* name, SMs, clocks  */
+
+/*
+ * Batched lower-bound searches: exactly the SEARCHES registry
+ * (lowerbound.py:321-381; raw cores lowerbound.py:88-308) for n independent
+ * problems {b - a*x mod 1 : x < count} at word width W in {32, 64}.
+ * Inputs a, b, eps are the UFrac raws (< 2^W, eps < 2^(W-1)), count >= 1.
+ * Outputs: ok (Verdict.SUCCESS = 1), d raw, iterations (SearchOutcome
+ * .iterations, per-mode for the classic family), points_placed as
+ * points_lo + 2^64 * points_hi.  iterations may be NULL.
+ */
+int hrb_search_batch(int algo, int mode, int word_bits, int64_t n, const uint64_t* a,
+                     const uint64_t* b, const uint64_t* eps, const uint64_t* count, uint8_t* ok,
+                     uint64_t* d, uint64_t* iterations, uint64_t* points_lo, uint8_t* points_hi,
+                     void* stream);
+
+/*
+ * A slice: S consecutive super-domains of one output-exponent piece run,
+ * packed by the host after taylor_approx + hierarchical_split
+ * (polygen.py:113-131, 193-252).  All arrays are device pointers, SoA.
+ *
+ *   coef    uint32[6][coef_limbs][S]  two's complement little-endian limbs of
+ *           the binomial-basis coefficients of r_0 (3), r_1 (2), r_2 (1) in
+ *           the packet variable i (hierarchical_split output), in the order
+ *           r0.c0 r0.c1 r0.c2 r1.c0 r1.c1 r2.c0 (unused ones zero for delta=1)
+ *   G       uint64[2][S]   ceil(eps' * 2^F) (lo, hi), eps' = eps + eps_approx
+ *   s2abs   uint64[2][S]   |r2.c0| saturated to 2^128-1 (delta=2), else 0
+ *   n_dom   uint32[S]      domains in the super-domain (tau_t)
+ *   dom_n   uint32[S]      domain size N_t
+ *   last_n  uint32[S]      size of the last domain (ragged tail)
+ *   dom_base uint64[S+1]   exclusive prefix sum of n_dom (slice-local ids)
+ *   m0      uint64[S]      binade index of the super-domain's first argument
+ *
+ * Host guarantees (checked in the Python layer, pipeline.py:178-184 and
+ * fpmodel.py:220-225 semantics): W <= F <= 128, 1 <= delta <= 2, and for
+ * every count used eps'' < 1/4 and 2*pad < 2^(W-1).
+ */
+typedef struct hrb_slice {
+    int64_t n_super;
+    int64_t n_total;    /* sum of n_dom (host scalar: sizes device scratch)   */
+    uint32_t max_dom_n; /* max of dom_n and last_n (host scalar)              */
+    int32_t coef_limbs;
+    int32_t frac_bits;
+    int32_t word_bits;
+    int32_t delta;
+    const uint32_t* coef;
+    const uint64_t* G;
+    const uint64_t* s2abs;
+    const uint32_t* n_dom;
+    const uint32_t* dom_n;
+    const uint32_t* last_n;
+    const uint64_t* dom_base;
+    const uint64_t* m0;
+} hrb_slice;
+
+/*
+ * Tabulated differences (polygen.py:134-158, 255-280 domain_coefficient_sets):
+ * per-domain coefficient sets (s0, s1, s2) = (r0(i), r1(i), r2(i)) for every
+ * domain of the slice, walked with add-with-carry chains from per-packet
+ * seeds.  out: uint32[3][coef_limbs][n_total] two's complement (exact while
+ * the values fit coef_limbs limbs; the host checks the MPInt budget).
+ */
+int hrb_domain_coefficients(const hrb_slice* s, uint32_t* out, void* stream);
+
+/*
+ * Phase 1 (pipeline.py:213-231), fused: tabulated walk -> degree-1 Boolean
+ * problem (pipeline.py:141-175) -> search -> warp-aggregated compaction of
+ * failing slice-local domain ids.  fail_ids receives the ids in ascending
+ * order (sorted on the device), *fail_count (device u64) the true count.
+ * iter_sum (device u64, may be NULL) accumulates SearchOutcome.iterations.
+ */
+int hrb_phase1(const hrb_slice* s, int algo, int mode, uint64_t* fail_ids, uint64_t* fail_count,
+               uint64_t cap, uint64_t* iter_sum, void* stream);
+
+/*
+ * Phase 2 (pipeline.py:234-257): for each failing domain, split `split`
+ * ways (2..64), Taylor-shift to each subdomain start, re-test.  Input: the
+ * n_fail ids of phase 1 (device count pointer).  Output keys
+ * (slice-local id << 8 | sub index), ascending.
+ */
+int hrb_phase2(const hrb_slice* s, int algo, int mode, int split, const uint64_t* fail_ids,
+               const uint64_t* fail_count, uint64_t fail_cap, uint64_t* sub_keys, uint64_t* sub_count,
+               uint64_t cap, void* stream);
+
+/*
+ * Phase 3 (pipeline.py:260-293): exact second-order walk of each surviving
+ * subdomain mod 2^F; arguments inside the eps' window become candidates:
+ * binade argument index, distance floored to 2^-64, slice-local domain id,
+ * ascending by argument.
+ */
+int hrb_phase3(const hrb_slice* s, int split, const uint64_t* sub_keys, const uint64_t* sub_count,
+               uint64_t sub_cap, uint64_t* cand_index, uint64_t* cand_dist, uint64_t* cand_dom,
+               uint64_t* cand_count, uint64_t cap, void* stream);
+
+/*
+ * The three phases back to back on the device (the north-star hot path for
+ * one slice); no host synchronisation between phases.  counts (device
+ * uint64[4]): phase-1 fails, phase-2 survivors, phase-3 candidates,
+ * phase-1 iteration sum.  Capacities: fail_cap, sub_cap, cand_cap.
+ */
+typedef struct hrb_run_out {
+    uint64_t* fail_ids;
+    uint64_t fail_cap;
+    uint64_t* sub_keys;
+    uint64_t sub_cap;
+    uint64_t* cand_index;
+    uint64_t* cand_dist;
+    uint64_t* cand_dom;
+    uint64_t cand_cap;
+    uint64_t* counts;
+} hrb_run_out;
+
+int hrb_run_slice(const hrb_slice* s, int algo, int mode, int split, const hrb_run_out* out,
+                  void* stream);
+
+/*
+ * End-to-end variant with HOST buffers (pageable or pinned): copies the
+ * slice to the device, runs hrb_run_slice, copies counts and candidates
+ * back, synchronises.  Host outputs: counts[4], fail_ids (<= fail_cap),
+ * cand_* (<= cand_cap).  Device buffers are cached per device and grown on
+ * demand (a too-small internal subdomain buffer triggers one re-run).
+ * device_ms (may be NULL) receives the kernel-only time of the last run.
+ */
+int hrb_run_slice_host(const hrb_slice* host_slice, int algo, int mode, int split,
+                       uint64_t* counts, uint64_t* fail_ids, uint64_t fail_cap,
+                       uint64_t* cand_index, uint64_t* cand_dist, uint64_t* cand_dom,
+                       uint64_t cand_cap, float* device_ms);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HRB200_H */

@@ -1,0 +1,114 @@
+"""hardround-b200: B200-native (sm_100a) hard-to-round case search.
+
+A drop-in for the reference `hardround` package's hot path
+(/root/reference/pkg/src/hardround/__init__.py:62-114 export list): the same
+public names, with the searches, the tabulated coefficient walk, the three
+filtering phases and all compaction executed by hand-written CUDA kernels
+behind the C-ABI of include/hrb200.h.  Rigorous Taylor models, error
+budgets and candidate confirmation stay on the host (mpmath), as in the
+paper's hybrid CPU-GPU split.
+"""
+
+from .arith import DivisionMode, MPInt, MPOverflowError, UFrac, frac_div
+from .enclosure import UndecidedError, decide_hr, derivative_bound, enclose, value_exponent
+from .fpformat import (
+    BinadeDomains,
+    Domain,
+    ErrorBudget,
+    FpFormat,
+    HrCaseRecord,
+    bits_float,
+    dist_p,
+    float_bits,
+    is_hr_case,
+    mantissa_exponent,
+    split_binade,
+)
+from .funnel import (
+    DomainTask,
+    PhaseConfig,
+    PhaseRow,
+    PhaseStats,
+    PipelineConfig,
+    SubdomainTask,
+    phase1,
+    phase2,
+    phase3_exhaustive,
+    prepare_slice,
+    execute_batch,
+    run_pipeline,
+    run_slice,
+    select_algorithm,
+)
+from .search import (
+    SEARCHES,
+    Algorithm,
+    SearchOutcome,
+    SearchProblem,
+    Verdict,
+    lefevre_lb,
+    lefevre_swap_lb,
+    regular_lb,
+    regular_unrolled_lb,
+    search_many,
+)
+from .slices import SliceBatch, SuperDomain, build_super_domains, output_binade_pieces, pack_slice
+from .taylor import (
+    BinomialPoly,
+    PolyGenConfig,
+    forward_difference,
+    hierarchical_split,
+    newton_interpolate,
+    straightforward_shift,
+    tabulated_shift_step,
+    taylor_approx,
+)
+
+__version__ = "0.1.0"
+
+
+def domain_coefficient_sets(r_polys, cfg: PolyGenConfig) -> list[tuple]:
+    """Per-domain coefficient tuples (s_0..s_delta) of one super-domain
+    (polygen.py:274-280), walked on the GPU (hrb_domain_coefficients)."""
+    from .device import DeviceSlice, domain_coefficients
+    from .arith import as_int
+    from fractions import Fraction
+
+    sd = SuperDomain(0, cfg.tau * cfg.N, cfg.N, cfg.tau, cfg.mu, cfg.nu, 0, 0, tuple(r_polys), Fraction(0))
+    pg = PolyGenConfig(tau=cfg.tau, N=cfg.N, mu=cfg.mu, nu=cfg.nu, delta=2, limbs=cfg.limbs,
+                       frac_bits=max(cfg.frac_bits, 64), guard=cfg.guard)
+    padded = list(r_polys) + [BinomialPoly((0,))] * (3 - len(r_polys))
+    batch = pack_slice([SuperDomain(0, sd.count, sd.n_p, sd.tau, sd.mu, sd.nu, 0, 0, tuple(padded), Fraction(0))],
+                       FpFormat(53, 32), pg, 64, 0, check=False)
+    from .slices import _walk_bound, _emulate_walk
+
+    if _walk_bound(sd) >> (32 * cfg.limbs):
+        _emulate_walk(sd, cfg.limbs)
+    raw = domain_coefficients(DeviceSlice(batch))
+    cl = raw.shape[1]
+    out = []
+    for i in range(cfg.tau):
+        vals = []
+        for j in range(len(r_polys)):
+            v = 0
+            for l in range(cl):
+                v |= int(raw[j, l, i]) << (32 * l)
+            if v >> (32 * cl - 1):
+                v -= 1 << (32 * cl)
+            vals.append(MPInt.from_int(v, cfg.limbs))
+        out.append(tuple(vals))
+    return out
+
+
+__all__ = [
+    "Algorithm", "BinadeDomains", "BinomialPoly", "DivisionMode", "Domain", "DomainTask", "ErrorBudget",
+    "FpFormat", "HrCaseRecord", "MPInt", "MPOverflowError", "PhaseConfig", "PhaseRow", "PhaseStats",
+    "PipelineConfig", "PolyGenConfig", "SEARCHES", "SearchOutcome", "SearchProblem", "SliceBatch",
+    "SubdomainTask", "SuperDomain", "UFrac", "UndecidedError", "Verdict", "bits_float", "build_super_domains",
+    "decide_hr", "derivative_bound", "dist_p", "domain_coefficient_sets", "enclose", "execute_batch",
+    "float_bits", "forward_difference", "frac_div", "hierarchical_split", "is_hr_case", "lefevre_lb",
+    "lefevre_swap_lb", "mantissa_exponent", "newton_interpolate", "output_binade_pieces", "pack_slice",
+    "phase1", "phase2", "phase3_exhaustive", "prepare_slice", "regular_lb", "regular_unrolled_lb",
+    "run_pipeline", "run_slice", "search_many", "select_algorithm", "split_binade", "straightforward_shift",
+    "tabulated_shift_step", "taylor_approx", "value_exponent",
+]

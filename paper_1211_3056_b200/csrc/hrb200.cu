@@ -1,0 +1,1018 @@
+// hrb200.cu -- sm_100a kernels + C-ABI of the HR-case search hot path.
+//
+// Pipeline (reference /root/reference/pkg/src/hardround/pipeline.py:412-463,
+// phases 213-293) for one slice of super-domains, entirely on the device:
+//
+//   prep      per super-domain: warp tiles, max subdomain count, max step
+//   phase1    fused tabulated walk (polygen.py:134-158, 255-280) -> degree-1
+//             Boolean problem (pipeline.py:141-175) -> search (lowerbound.py)
+//             -> verdict bits transposed into a domain bitmap with __ballot_sync
+//   compact1  ordered popc-scan compaction of the bitmap -> failing ids
+//   phase2    per (failing domain, subdomain): Toeplitz shift + re-test -> bitmap
+//   compact2  ordered compaction -> surviving subdomain keys
+//   phase3    per (subdomain, chunk): second-order walk mod 2^F, window test,
+//             warp-aggregated atomic append (__ballot_sync/__popc, one atomic
+//             per warp) + per-thread candidate counts
+//   scatter3  scan of the counts turns the unordered append into the
+//             reference's argument order (deterministic, no sort)
+//
+// Data layout: see include/hrb200.h.  All counts between phases stay on the
+// device (grid-stride kernels read them), so a slice runs without host
+// synchronisation until the caller reads the counts.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <cub/cub.cuh>
+#include <mutex>
+#include <string>
+
+#include "../../include/hrb200.h"
+#include "search_core.cuh"
+
+using u128 = unsigned __int128;
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const char* msg) {
+    g_err = msg;
+    return code;
+}
+
+int cuda_err(cudaError_t e, const char* where) {
+    if (e == cudaSuccess) return HRB_OK;
+    g_err = std::string(where) + ": " + cudaGetErrorString(e);
+    return HRB_ERR_RUNTIME;
+}
+
+#define CK(x)                                          \
+    do {                                               \
+        int _rc = cuda_err((x), #x);                   \
+        if (_rc) return _rc;                           \
+    } while (0)
+
+constexpr int NU = 16;             // domains per lane in phase 1 (stride-32 walk)
+constexpr int TILE = 32 * NU;      // domains per warp tile
+constexpr int CHUNK3 = 256;        // arguments per thread in phase 3
+constexpr int SCAN_BLOCKS = 592;   // 4 CTAs per SM on 148 SMs
+constexpr int SCAN_THREADS = 256;
+
+// ---------------------------------------------------------------------------
+// slice view on the device
+// ---------------------------------------------------------------------------
+struct SliceDev {
+    int64_t S;
+    int CL, F, W, delta;
+    const uint32_t* coef;
+    const uint64_t* G;
+    const uint64_t* s2abs;
+    const uint32_t* n_dom;
+    const uint32_t* dom_n;
+    const uint32_t* last_n;
+    const uint64_t* dom_base;
+    const uint64_t* m0;
+};
+
+SliceDev to_dev(const hrb_slice* s) {
+    SliceDev d;
+    d.S = s->n_super;
+    d.CL = s->coef_limbs;
+    d.F = s->frac_bits;
+    d.W = s->word_bits;
+    d.delta = s->delta;
+    d.coef = s->coef;
+    d.G = s->G;
+    d.s2abs = s->s2abs;
+    d.n_dom = s->n_dom;
+    d.dom_n = s->dom_n;
+    d.last_n = s->last_n;
+    d.dom_base = s->dom_base;
+    d.m0 = s->m0;
+    return d;
+}
+
+__device__ __forceinline__ u128 mask_f(int F) { return F >= 128 ? ~(u128)0 : (((u128)1 << F) - 1); }
+
+// residue mod 2^128 of packed coefficient c of super-domain t
+__device__ __forceinline__ u128 coef_res(const SliceDev& s, int64_t t, int c) {
+    u128 r = 0;
+    int lim = s.CL < 4 ? s.CL : 4;
+    for (int l = 0; l < lim; l++) r |= (u128)__ldg(&s.coef[((int64_t)c * s.CL + l) * s.S + t]) << (32 * l);
+    if (s.CL < 4 && (__ldg(&s.coef[((int64_t)c * s.CL + s.CL - 1) * s.S + t]) & 0x80000000u)) {
+        r |= ~(u128)0 << (32 * s.CL);  // sign-extend
+    }
+    return r;
+}
+
+__device__ __forceinline__ u128 ld128(const uint64_t* p, int64_t S, int64_t t) {
+    return ((u128)__ldg(&p[S + t]) << 64) | __ldg(&p[t]);
+}
+
+// pad of pipeline.py:165-166: ceil((G + |s2| (n-1)^2) / 2^(F-W)) + n + 1
+__device__ __forceinline__ uint64_t pad_of(u128 G, u128 s2abs, uint64_t n, int F, int W) {
+    uint64_t nm1 = n - 1;
+    u128 X = G + s2abs * (u128)(nm1 * nm1);
+    int sh = F - W;
+    u128 q = sh > 0 ? (X >> sh) + ((X & ((((u128)1) << sh) - 1)) != 0) : X;
+    return (uint64_t)q + n + 1;
+}
+
+struct Problem {
+    uint64_t a, b, eps;
+};
+
+// _boolean_problem (pipeline.py:149-175) from residues of s0, s1
+__device__ __forceinline__ Problem make_problem(u128 s0, u128 s1, uint64_t pad, int F, int W, u128 mF) {
+    Problem p;
+    u128 s0m = s0 & mF;
+    u128 s1m = (0 - s1) & mF;
+    uint64_t wmask = W == 64 ? ~0ull : ((1ull << W) - 1);
+    p.a = (uint64_t)(s1m >> (F - W));
+    p.b = ((uint64_t)(s0m >> (F - W)) + pad) & wmask;
+    p.eps = 2 * pad;
+    return p;
+}
+
+// largest t with base[t] <= x, base ascending of length S+1
+__device__ __forceinline__ int64_t find_seg(const uint64_t* base, int64_t S, uint64_t x) {
+    int64_t lo = 0, hi = S - 1;
+    while (lo < hi) {
+        int64_t mid = (lo + hi + 1) >> 1;
+        if (__ldg(&base[mid]) <= x) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ uint64_t domain_size(const SliceDev& s, int64_t t, uint64_t i) {
+    uint32_t nd = __ldg(&s.n_dom[t]);
+    return i == (uint64_t)nd - 1 ? __ldg(&s.last_n[t]) : __ldg(&s.dom_n[t]);
+}
+
+__device__ __forceinline__ uint64_t binom2(uint64_t i) { return i ? (i * (i - 1)) >> 1 : 0; }
+
+// run one search to completion; REG selects the family at compile time so a
+// kernel instantiation carries only one loop body (register pressure)
+template <int W, bool REG>
+__device__ __forceinline__ hrb::Outcome search_one(int algo, int mode, const Problem& p, uint64_t n) {
+    if (REG) {
+        hrb::Outcome o = hrb::regular_search<W>(p.a, p.b, p.eps, n);
+        if (algo == hrb::ALGO_REGULAR_UNROLLED) o.it = (o.it + 1) >> 1;
+        return o;
+    }
+    return hrb::lefevre_search<W>(p.a, p.b, p.eps, n, mode);
+}
+
+// ---------------------------------------------------------------------------
+// prep: tiles per super-domain, max subdomain count J, max subdomain step
+// ---------------------------------------------------------------------------
+__global__ void prep_kernel(SliceDev s, int split, uint64_t* tiles, unsigned long long* meta) {
+    int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t > s.S) return;
+    if (t == s.S) {
+        tiles[t] = 0;
+        return;
+    }
+    uint32_t nd = s.n_dom[t];
+    tiles[t] = (nd + TILE - 1) / TILE;
+    uint64_t sizes[2] = {s.dom_n[t], s.last_n[t]};
+    unsigned long long J = 0, mstep = 0;
+    for (int k = 0; k < 2; k++) {
+        uint64_t n = sizes[k];
+        uint64_t step = n / split;
+        if (step < 1) step = 1;
+        uint64_t nsub = (n + step - 1) / step;
+        if (nsub > J) J = nsub;
+        if (step > mstep) mstep = step;
+    }
+    atomicMax(&meta[0], J);
+    atomicMax(&meta[1], mstep);
+}
+
+// ---------------------------------------------------------------------------
+// phase 1: fused tabulated walk + Boolean test, verdict bitmap
+// ---------------------------------------------------------------------------
+template <int W, bool REG>
+__global__ void __launch_bounds__(256) phase1_kernel(SliceDev s, int algo, int mode, const uint64_t* tile_base,
+                                                     uint32_t* bitmap, unsigned long long* iter_sum) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const uint64_t total_tiles = tile_base[s.S];
+    const u128 mF = mask_f(s.F);
+    unsigned long long iters = 0;
+    for (uint64_t gw = warp0; gw < total_tiles; gw += nwarps) {
+        const int64_t t = find_seg(tile_base, s.S, gw);
+        const uint64_t tile = gw - tile_base[t];
+        const uint32_t nd = __ldg(&s.n_dom[t]);
+        const u128 c00 = coef_res(s, t, 0), c01 = coef_res(s, t, 1), c02 = coef_res(s, t, 2);
+        const u128 c10 = coef_res(s, t, 3), c11 = coef_res(s, t, 4);
+        const u128 G = ld128(s.G, s.S, t);
+        const u128 s2a = s.delta >= 2 ? ld128(s.s2abs, s.S, t) : (u128)0;
+        const uint64_t nfull = __ldg(&s.dom_n[t]), nlast = __ldg(&s.last_n[t]);
+        const uint64_t pad_full = pad_of(G, s2a, nfull, s.F, W);
+        const uint64_t pad_last = pad_of(G, s2a, nlast, s.F, W);
+        // seeds of the stride-32 difference tables at this lane's first domain
+        const uint64_t il = tile * TILE + lane;
+        u128 g0 = c00 + c01 * (u128)il + c02 * (u128)binom2(il);  // r0(il)
+        u128 g1 = (c01 << 5) + c02 * (u128)(32 * il + 496);       // r0(il+32) - r0(il)
+        const u128 g2 = c02 << 10;                                // second difference
+        u128 h0 = c10 + c11 * (u128)il;                           // r1(il)
+        const u128 h1 = c11 << 5;
+        uint32_t fails = 0;
+#pragma unroll 1
+        for (int k = 0; k < NU; k++) {
+            const uint64_t i = il + 32 * (uint64_t)k;
+            if (i < nd) {
+                const bool last = i == (uint64_t)nd - 1;
+                const uint64_t n = last ? nlast : nfull;
+                Problem p = make_problem(g0, h0, last ? pad_last : pad_full, s.F, W, mF);
+                hrb::Outcome o = search_one<W, REG>(algo, mode, p, n);
+                iters += o.it;
+                if (!o.ok) fails |= 1u << k;
+            }
+            g0 += g1;  // tabulated step: 3 multi-word additions per domain
+            g1 += g2;
+            h0 += h1;
+        }
+        uint32_t mine = 0;
+#pragma unroll
+        for (int k = 0; k < NU; k++) {
+            uint32_t w = __ballot_sync(0xffffffffu, (fails >> k) & 1u);
+            if (lane == k) mine = w;
+        }
+        if (lane < NU) bitmap[gw * NU + lane] = mine;
+    }
+    // warp-reduce the iteration count, one atomic per warp
+    for (int o = 16; o > 0; o >>= 1) iters += __shfl_xor_sync(0xffffffffu, iters, o);
+    if (iter_sum && lane == 0 && iters) atomicAdd(iter_sum, iters);
+}
+
+// ---------------------------------------------------------------------------
+// phase 2: per (failing domain, subdomain j): shift, re-test, bitmap
+// ---------------------------------------------------------------------------
+template <int W, bool REG>
+__global__ void __launch_bounds__(256) phase2_kernel(SliceDev s, int algo, int mode, int split,
+                                                     const uint64_t* fail_ids, const uint64_t* fail_count,
+                                                     uint64_t fail_cap, const unsigned long long* meta,
+                                                     uint32_t* bitmap) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t J = meta[0];
+    uint64_t nf = *fail_count;
+    if (nf > fail_cap) nf = fail_cap;
+    const uint64_t n_items = nf * J;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const u128 mF = mask_f(s.F);
+    for (uint64_t base = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) & ~31ull; base < n_items; base += stride) {
+        const uint64_t g = base + lane;
+        bool fail = false;
+        if (g < n_items) {
+            const uint64_t f = g / J, j = g - f * J;
+            const uint64_t id = fail_ids[f];
+            const int64_t t = find_seg(s.dom_base, s.S, id);
+            const uint64_t i = id - s.dom_base[t];
+            const uint64_t n = domain_size(s, t, i);
+            uint64_t step = n / split;
+            if (step < 1) step = 1;
+            const uint64_t nsub = (n + step - 1) / step;
+            if (j < nsub) {
+                const uint64_t start = j * step;
+                const uint64_t cnt = n - start < step ? n - start : step;
+                const u128 c00 = coef_res(s, t, 0), c01 = coef_res(s, t, 1), c02 = coef_res(s, t, 2);
+                const u128 c10 = coef_res(s, t, 3), c11 = coef_res(s, t, 4), c20 = coef_res(s, t, 5);
+                // domain polynomial (s0, s1, s2) at i, then straightforward_shift by start
+                const u128 s0 = c00 + c01 * (u128)i + c02 * (u128)binom2(i);
+                const u128 s1 = c10 + c11 * (u128)i;
+                const u128 s2 = s.delta >= 2 ? c20 : (u128)0;
+                const u128 t0 = s0 + s1 * (u128)start + s2 * (u128)binom2(start);
+                const u128 t1 = s1 + s2 * (u128)start;
+                const u128 G = ld128(s.G, s.S, t);
+                const u128 s2a = s.delta >= 2 ? ld128(s.s2abs, s.S, t) : (u128)0;
+                Problem p = make_problem(t0, t1, pad_of(G, s2a, cnt, s.F, W), s.F, W, mF);
+                hrb::Outcome o = search_one<W, REG>(algo, mode, p, cnt);
+                fail = !o.ok;
+            }
+        }
+        uint32_t w = __ballot_sync(0xffffffffu, fail);
+        if (lane == 0 && base < n_items) bitmap[base >> 5] = w;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// phase 3: exhaustive second-order walk of surviving subdomains
+// ---------------------------------------------------------------------------
+struct Cand {
+    uint64_t m, dist, dom, item;
+    uint32_t rank;
+};
+
+__global__ void __launch_bounds__(256) phase3_kernel(SliceDev s, int split, const uint64_t* sub_keys,
+                                                     const uint64_t* sub_count, uint64_t sub_cap,
+                                                     const unsigned long long* meta, uint32_t* item_counts,
+                                                     Cand* app, unsigned long long* app_count, uint64_t app_cap) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t maxstep = meta[1];
+    const uint64_t CH = (maxstep + CHUNK3 - 1) / CHUNK3;
+    uint64_t ns = *sub_count;
+    if (ns > sub_cap) ns = sub_cap;
+    const uint64_t n_items = ns * CH;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const int F = s.F;
+    const u128 mF = mask_f(F);
+    const u128 oneF = F >= 128 ? (u128)0 : ((u128)1 << F);
+    for (uint64_t base = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) & ~31ull; base < n_items; base += stride) {
+        const uint64_t g = base + lane;
+        uint64_t len = 0, mbase = 0, dom = 0;
+        u128 v = 0, d1 = 0, d2 = 0, window = 1;
+        if (g < n_items) {
+            const uint64_t r = g / CH, c = g - r * CH;
+            const uint64_t key = sub_keys[r];
+            dom = key >> 8;
+            const uint64_t j = key & 255;
+            const int64_t t = find_seg(s.dom_base, s.S, dom);
+            const uint64_t i = dom - s.dom_base[t];
+            const uint64_t n = domain_size(s, t, i);
+            uint64_t step = n / split;
+            if (step < 1) step = 1;
+            const uint64_t start = j * step;
+            const uint64_t cnt = n - start < step ? n - start : step;
+            const uint64_t x0 = c * CHUNK3;
+            if (x0 < cnt) {
+                len = cnt - x0 < CHUNK3 ? cnt - x0 : CHUNK3;
+                const uint64_t o = start + x0;
+                const u128 c00 = coef_res(s, t, 0), c01 = coef_res(s, t, 1), c02 = coef_res(s, t, 2);
+                const u128 c10 = coef_res(s, t, 3), c11 = coef_res(s, t, 4), c20 = coef_res(s, t, 5);
+                const u128 s0 = c00 + c01 * (u128)i + c02 * (u128)binom2(i);
+                const u128 s1 = c10 + c11 * (u128)i;
+                const u128 s2 = s.delta >= 2 ? c20 : (u128)0;
+                v = s0 + s1 * (u128)o + s2 * (u128)binom2(o);  // P(o)
+                d1 = s1 + s2 * (u128)o;                        // Delta P(o)
+                d2 = s2;
+                window = ld128(s.G, s.S, t) + 1;  // ceil(eps' 2^F) + 1  (pipeline.py:274)
+                mbase = __ldg(&s.m0[t]) + i * (uint64_t)__ldg(&s.dom_n[t]) + o;
+            }
+        }
+        const u128 hiw = (oneF - window) & mF;
+        uint32_t rank = 0;
+        for (int x = 0; x < CHUNK3; x++) {
+            const u128 vm = v & mF;
+            const bool hit = (uint64_t)x < len && (vm < window || vm > hiw);
+            if (__any_sync(0xffffffffu, hit)) {
+                const uint32_t ball = __ballot_sync(0xffffffffu, hit);
+                const int leader = __ffs(ball) - 1;
+                unsigned long long pos = 0;
+                if (lane == leader) pos = atomicAdd(app_count, (unsigned long long)__popc(ball));
+                pos = __shfl_sync(0xffffffffu, pos, leader);
+                if (hit) {
+                    pos += __popc(ball & ((1u << lane) - 1));
+                    if (pos < app_cap) {
+                        const u128 comp = (oneF - vm) & mF;
+                        const u128 dist = (vm == 0 || vm < comp) ? vm : comp;
+                        Cand cd;
+                        cd.m = mbase + x;
+                        cd.dist = F >= 64 ? (uint64_t)(dist >> (F - 64)) : (uint64_t)(dist << (64 - F));
+                        cd.dom = dom;
+                        cd.item = g;
+                        cd.rank = rank;
+                        app[pos] = cd;
+                    }
+                    rank++;
+                }
+            }
+            v += d1;
+            d1 += d2;
+        }
+        if (g < n_items) item_counts[g] = rank;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// ordered compaction: 3-kernel reduce / scan / scatter with a device-side size
+// ---------------------------------------------------------------------------
+struct P1Compact {  // bitmap of padded domain indices -> slice-local ids
+    const uint32_t* bm;
+    const uint64_t* tile_base;
+    const uint64_t* dom_base;
+    int64_t S;
+    uint64_t* out;
+    uint64_t cap;
+    __device__ uint64_t size() const { return tile_base[S] * NU; }
+    __device__ uint32_t count(uint64_t w) const { return __popc(bm[w]); }
+    __device__ void emit(uint64_t w, uint64_t off) const {
+        uint32_t x = bm[w];
+        while (x) {
+            int b = __ffs(x) - 1;
+            x &= x - 1;
+            if (off < cap) {
+                uint64_t P = w * 32 + b;
+                uint64_t gw = P / TILE;
+                int64_t t = find_seg(tile_base, S, gw);
+                out[off] = dom_base[t] + (P - tile_base[t] * TILE);
+            }
+            off++;
+        }
+    }
+};
+
+struct P2Compact {  // bitmap over (f, j) items -> (id << 8 | j)
+    const uint32_t* bm;
+    const uint64_t* fail_ids;
+    const uint64_t* fail_count;
+    uint64_t fail_cap;
+    const unsigned long long* meta;
+    uint64_t* out;
+    uint64_t cap;
+    __device__ uint64_t size() const {
+        uint64_t nf = *fail_count;
+        if (nf > fail_cap) nf = fail_cap;
+        return (nf * meta[0] + 31) >> 5;
+    }
+    __device__ uint32_t count(uint64_t w) const { return __popc(bm[w]); }
+    __device__ void emit(uint64_t w, uint64_t off) const {
+        uint32_t x = bm[w];
+        const uint64_t J = meta[0];
+        while (x) {
+            int b = __ffs(x) - 1;
+            x &= x - 1;
+            if (off < cap) {
+                uint64_t g = w * 32 + b;
+                uint64_t f = g / J;
+                out[off] = (fail_ids[f] << 8) | (g - f * J);
+            }
+            off++;
+        }
+    }
+};
+
+struct P3Offsets {  // per-item candidate counts -> per-item output offsets
+    const uint32_t* counts;
+    const uint64_t* sub_count;
+    uint64_t sub_cap;
+    const unsigned long long* meta;
+    uint64_t* offs;
+    __device__ uint64_t size() const {
+        uint64_t ns = *sub_count;
+        if (ns > sub_cap) ns = sub_cap;
+        return ns * ((meta[1] + CHUNK3 - 1) / CHUNK3);
+    }
+    __device__ uint32_t count(uint64_t i) const { return counts[i]; }
+    __device__ void emit(uint64_t i, uint64_t off) const { offs[i] = off; }
+};
+
+template <class Fn>
+__global__ void __launch_bounds__(SCAN_THREADS) scan_reduce_kernel(Fn fn, uint64_t* block_sums) {
+    using BR = cub::BlockReduce<unsigned long long, SCAN_THREADS>;
+    __shared__ typename BR::TempStorage tmp;
+    const uint64_t n = fn.size();
+    const uint64_t chunk = (n + gridDim.x - 1) / gridDim.x;
+    const uint64_t lo = blockIdx.x * chunk, hi = lo + chunk < n ? lo + chunk : n;
+    unsigned long long acc = 0;
+    for (uint64_t i = lo + threadIdx.x; i < hi; i += SCAN_THREADS) acc += fn.count(i);
+    unsigned long long tot = BR(tmp).Sum(acc);
+    if (threadIdx.x == 0) block_sums[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(1024) scan_blocks_kernel(uint64_t* block_sums, int nb, uint64_t* total) {
+    using BS = cub::BlockScan<unsigned long long, 1024>;
+    __shared__ typename BS::TempStorage tmp;
+    unsigned long long v = threadIdx.x < nb ? block_sums[threadIdx.x] : 0, excl, agg;
+    BS(tmp).ExclusiveSum(v, excl, agg);
+    if (threadIdx.x < nb) block_sums[threadIdx.x] = excl;
+    if (threadIdx.x == 0) *total = agg;
+}
+
+template <class Fn>
+__global__ void __launch_bounds__(SCAN_THREADS) scan_scatter_kernel(Fn fn, const uint64_t* block_offs) {
+    using BS = cub::BlockScan<unsigned long long, SCAN_THREADS>;
+    __shared__ typename BS::TempStorage tmp;
+    const uint64_t n = fn.size();
+    const uint64_t chunk = (n + gridDim.x - 1) / gridDim.x;
+    const uint64_t lo = blockIdx.x * chunk, hi = lo + chunk < n ? lo + chunk : n;
+    unsigned long long run = block_offs[blockIdx.x];
+    for (uint64_t base = lo; base < hi; base += SCAN_THREADS) {
+        const uint64_t i = base + threadIdx.x;
+        unsigned long long c = i < hi ? fn.count(i) : 0, excl, agg;
+        BS(tmp).ExclusiveSum(c, excl, agg);
+        if (i < hi && c) fn.emit(i, run + excl);
+        run += agg;
+        __syncthreads();
+    }
+}
+
+__global__ void scatter3_kernel(const Cand* app, const unsigned long long* app_count, uint64_t app_cap,
+                                const uint64_t* offs, uint64_t* out_m, uint64_t* out_dist, uint64_t* out_dom,
+                                uint64_t cap) {
+    uint64_t n = *app_count;
+    if (n > app_cap) n = app_cap;
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n; k += (uint64_t)gridDim.x * blockDim.x) {
+        const Cand c = app[k];
+        const uint64_t pos = offs[c.item] + c.rank;
+        if (pos < cap) {
+            out_m[pos] = c.m;
+            out_dist[pos] = c.dist;
+            out_dom[pos] = c.dom;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// full-width tabulated differences (domain_coefficient_sets parity)
+// ---------------------------------------------------------------------------
+// x += y over CL limbs with one add-with-carry chain (IADD3 / IADD3.X)
+template <int CL>
+__device__ __forceinline__ void addc_chain(uint32_t (&x)[CL], const uint32_t (&y)[CL]) {
+    asm("add.cc.u32 %0, %0, %1;" : "+r"(x[0]) : "r"(y[0]));
+#pragma unroll
+    for (int l = 1; l < CL - 1; l++) asm("addc.cc.u32 %0, %0, %1;" : "+r"(x[l]) : "r"(y[l]));
+    if (CL > 1) asm("addc.u32 %0, %0, %1;" : "+r"(x[CL - 1]) : "r"(y[CL - 1]));
+}
+
+// r = x * m (mod 2^(32 CL)), two's complement x, unsigned 64-bit m
+template <int CL>
+__device__ __forceinline__ void mul_u64(uint32_t (&r)[CL], const uint32_t (&x)[CL], uint64_t m) {
+    uint32_t acc[CL];
+#pragma unroll
+    for (int l = 0; l < CL; l++) acc[l] = 0;
+    const uint32_t mw[2] = {(uint32_t)m, (uint32_t)(m >> 32)};
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+        uint64_t carry = 0;
+#pragma unroll
+        for (int l = 0; l + h < CL; l++) {
+            uint64_t p = (uint64_t)x[l] * mw[h] + acc[l + h] + carry;
+            acc[l + h] = (uint32_t)p;
+            carry = p >> 32;
+        }
+    }
+#pragma unroll
+    for (int l = 0; l < CL; l++) r[l] = acc[l];
+}
+
+template <int CL>
+__device__ __forceinline__ void load_coef_full(const SliceDev& s, int64_t t, int c, uint32_t (&x)[CL]) {
+#pragma unroll
+    for (int l = 0; l < CL; l++) x[l] = __ldg(&s.coef[((int64_t)c * CL + l) * s.S + t]);
+}
+
+template <int CL>
+__global__ void __launch_bounds__(128) tabdiff_full_kernel(SliceDev s, const uint64_t* tile_base, int64_t n_total,
+                                                          uint32_t* out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const uint64_t total_tiles = tile_base[s.S];
+    for (uint64_t gw = warp0; gw < total_tiles; gw += nwarps) {
+        const int64_t t = find_seg(tile_base, s.S, gw);
+        const uint64_t tile = gw - tile_base[t];
+        const uint32_t nd = __ldg(&s.n_dom[t]);
+        const uint64_t il = tile * TILE + lane;
+        uint32_t c[6][CL];
+#pragma unroll
+        for (int k = 0; k < 6; k++) load_coef_full<CL>(s, t, k, c[k]);
+        // column[j][l]: l-th stride-32 difference of r_j at the lane's domain
+        uint32_t g0[CL], g1[CL], g2[CL], h0[CL], h1[CL], z[CL], tmp[CL];
+        // g0 = c00 + c01*il + c02*C(il,2)
+#pragma unroll
+        for (int l = 0; l < CL; l++) g0[l] = c[0][l];
+        mul_u64<CL>(tmp, c[1], il);
+        addc_chain<CL>(g0, tmp);
+        mul_u64<CL>(tmp, c[2], binom2(il));
+        addc_chain<CL>(g0, tmp);
+        // g1 = 32 c01 + c02 (32 il + 496);  g2 = 1024 c02
+        mul_u64<CL>(g1, c[1], 32);
+        mul_u64<CL>(tmp, c[2], 32 * il + 496);
+        addc_chain<CL>(g1, tmp);
+        mul_u64<CL>(g2, c[2], 1024);
+        // h0 = c10 + c11 il;  h1 = 32 c11
+#pragma unroll
+        for (int l = 0; l < CL; l++) h0[l] = c[3][l];
+        mul_u64<CL>(tmp, c[4], il);
+        addc_chain<CL>(h0, tmp);
+        mul_u64<CL>(h1, c[4], 32);
+#pragma unroll
+        for (int l = 0; l < CL; l++) z[l] = s.delta >= 2 ? c[5][l] : 0u;
+        const uint64_t gbase = s.dom_base[t];
+        for (int k = 0; k < NU; k++) {
+            const uint64_t i = il + 32 * (uint64_t)k;
+            if (i < nd) {
+                const uint64_t gi = gbase + i;
+#pragma unroll
+                for (int l = 0; l < CL; l++) {
+                    out[((int64_t)0 * CL + l) * n_total + gi] = g0[l];
+                    out[((int64_t)1 * CL + l) * n_total + gi] = h0[l];
+                    out[((int64_t)2 * CL + l) * n_total + gi] = z[l];
+                }
+            }
+            addc_chain<CL>(g0, g1);
+            addc_chain<CL>(g1, g2);
+            addc_chain<CL>(h0, h1);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// search batch
+// ---------------------------------------------------------------------------
+template <int W, bool REG>
+__global__ void __launch_bounds__(256) search_batch_kernel(int algo, int mode, int64_t n, const uint64_t* a,
+                                                           const uint64_t* b, const uint64_t* eps,
+                                                           const uint64_t* count, uint8_t* ok, uint64_t* d,
+                                                           uint64_t* it, uint64_t* pl, uint8_t* ph) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        Problem p{a[i], b[i], eps[i]};
+        hrb::Outcome o = search_one<W, REG>(algo, mode, p, count[i]);
+        ok[i] = o.ok;
+        d[i] = o.d;
+        if (it) it[i] = o.it;
+        pl[i] = o.pts_lo;
+        ph[i] = (uint8_t)o.pts_hi;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// workspace (per device, grows; guarded by a mutex)
+// ---------------------------------------------------------------------------
+struct Buf {
+    void* p = nullptr;
+    size_t n = 0;
+    int ensure(size_t bytes) {
+        if (bytes <= n) return HRB_OK;
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+        size_t want = bytes + bytes / 4 + 256;
+        CK(cudaMalloc(&p, want));
+        n = want;
+        return HRB_OK;
+    }
+};
+
+struct Workspace {
+    Buf tiles, tile_base, meta, bm1, bm2, blocks, total, counts3, offs3, app, appc, cub_tmp, fail_cnt_tmp;
+};
+
+std::mutex g_ws_mu;
+Workspace g_ws[64];
+
+int current_ws(Workspace** out) {
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    *out = &g_ws[dev & 63];
+    return HRB_OK;
+}
+
+int sm_count() {
+    static int cached[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!cached[dev & 63]) {
+        int v = 148;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        cached[dev & 63] = v;
+    }
+    return cached[dev & 63];
+}
+
+int check_slice(const hrb_slice* s) {
+    if (!s) return set_err(HRB_ERR_CONFIG, "null slice");
+    if (s->n_super < 1) return set_err(HRB_ERR_CONFIG, "slice has no super-domains");
+    if (s->word_bits != 32 && s->word_bits != 64) return set_err(HRB_ERR_CONFIG, "word_bits must be 32 or 64");
+    if (s->frac_bits < s->word_bits || s->frac_bits > 128)
+        return set_err(HRB_ERR_CONFIG, "frac_bits must satisfy word_bits <= F <= 128");
+    if (s->delta < 1 || s->delta > 2) return set_err(HRB_ERR_CONFIG, "delta must be 1 or 2");
+    if (s->coef_limbs < 1 || s->coef_limbs > 16) return set_err(HRB_ERR_CONFIG, "coef_limbs outside [1, 16]");
+    return HRB_OK;
+}
+
+int ws_prep(Workspace& ws, const SliceDev& sd, int split, cudaStream_t st) {
+    const int64_t S = sd.S;
+    int rc;
+    if ((rc = ws.tiles.ensure(sizeof(uint64_t) * (S + 1)))) return rc;
+    if ((rc = ws.tile_base.ensure(sizeof(uint64_t) * (S + 1)))) return rc;
+    if ((rc = ws.meta.ensure(sizeof(unsigned long long) * 4))) return rc;
+    CK(cudaMemsetAsync(ws.meta.p, 0, sizeof(unsigned long long) * 4, st));
+    prep_kernel<<<(unsigned)((S + 1 + 255) / 256), 256, 0, st>>>(sd, split, (uint64_t*)ws.tiles.p,
+                                                                 (unsigned long long*)ws.meta.p);
+    CK(cudaGetLastError());
+    size_t tmp_bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, (uint64_t*)ws.tiles.p, (uint64_t*)ws.tile_base.p, S + 1, st);
+    if ((rc = ws.cub_tmp.ensure(tmp_bytes))) return rc;
+    CK(cub::DeviceScan::ExclusiveSum(ws.cub_tmp.p, tmp_bytes, (uint64_t*)ws.tiles.p, (uint64_t*)ws.tile_base.p,
+                                     S + 1, st));
+    return HRB_OK;
+}
+
+template <class Fn>
+int run_compact(Workspace& ws, const Fn& fn, uint64_t* total, cudaStream_t st) {
+    int rc;
+    if ((rc = ws.blocks.ensure(sizeof(uint64_t) * SCAN_BLOCKS))) return rc;
+    scan_reduce_kernel<Fn><<<SCAN_BLOCKS, SCAN_THREADS, 0, st>>>(fn, (uint64_t*)ws.blocks.p);
+    scan_blocks_kernel<<<1, 1024, 0, st>>>((uint64_t*)ws.blocks.p, SCAN_BLOCKS, total);
+    scan_scatter_kernel<Fn><<<SCAN_BLOCKS, SCAN_THREADS, 0, st>>>(fn, (const uint64_t*)ws.blocks.p);
+    CK(cudaGetLastError());
+    return HRB_OK;
+}
+
+int phase1_impl(Workspace& ws, const hrb_slice* s, const SliceDev& sd, int algo, int mode, uint64_t* fail_ids,
+                uint64_t* fail_count, uint64_t cap, uint64_t* iter_sum, cudaStream_t st) {
+    int rc;
+    // upper bound of tiles: n_total/TILE + S
+    const uint64_t max_tiles = (uint64_t)s->n_total / TILE + (uint64_t)s->n_super + 1;
+    if ((rc = ws.bm1.ensure(sizeof(uint32_t) * max_tiles * NU))) return rc;
+    const int grid = sm_count() * 8;
+    const bool reg = algo >= hrb::ALGO_REGULAR;
+    auto tb = (const uint64_t*)ws.tile_base.p;
+    auto bm = (uint32_t*)ws.bm1.p;
+    auto is = (unsigned long long*)iter_sum;
+    if (sd.W == 64 && reg) phase1_kernel<64, true><<<grid, 256, 0, st>>>(sd, algo, mode, tb, bm, is);
+    else if (sd.W == 64) phase1_kernel<64, false><<<grid, 256, 0, st>>>(sd, algo, mode, tb, bm, is);
+    else if (reg) phase1_kernel<32, true><<<grid, 256, 0, st>>>(sd, algo, mode, tb, bm, is);
+    else phase1_kernel<32, false><<<grid, 256, 0, st>>>(sd, algo, mode, tb, bm, is);
+    CK(cudaGetLastError());
+    P1Compact fn{(const uint32_t*)ws.bm1.p, (const uint64_t*)ws.tile_base.p, s->dom_base, sd.S, fail_ids, cap};
+    return run_compact(ws, fn, fail_count, st);
+}
+
+int phase2_impl(Workspace& ws, const hrb_slice* s, const SliceDev& sd, int algo, int mode, int split,
+                const uint64_t* fail_ids, const uint64_t* fail_count, uint64_t fail_cap, uint64_t* sub_keys,
+                uint64_t* sub_count, uint64_t cap, cudaStream_t st) {
+    int rc;
+    const uint64_t Jmax = 2 * (uint64_t)split;
+    if ((rc = ws.bm2.ensure(sizeof(uint32_t) * ((fail_cap * Jmax + 31) / 32 + 1)))) return rc;
+    const int grid = sm_count() * 8;
+    const bool reg = algo >= hrb::ALGO_REGULAR;
+    auto mt = (const unsigned long long*)ws.meta.p;
+    auto bm = (uint32_t*)ws.bm2.p;
+    if (sd.W == 64 && reg)
+        phase2_kernel<64, true><<<grid, 256, 0, st>>>(sd, algo, mode, split, fail_ids, fail_count, fail_cap, mt, bm);
+    else if (sd.W == 64)
+        phase2_kernel<64, false><<<grid, 256, 0, st>>>(sd, algo, mode, split, fail_ids, fail_count, fail_cap, mt, bm);
+    else if (reg)
+        phase2_kernel<32, true><<<grid, 256, 0, st>>>(sd, algo, mode, split, fail_ids, fail_count, fail_cap, mt, bm);
+    else
+        phase2_kernel<32, false><<<grid, 256, 0, st>>>(sd, algo, mode, split, fail_ids, fail_count, fail_cap, mt, bm);
+    CK(cudaGetLastError());
+    P2Compact fn{(const uint32_t*)ws.bm2.p, fail_ids, fail_count, fail_cap, (const unsigned long long*)ws.meta.p,
+                 sub_keys, cap};
+    return run_compact(ws, fn, sub_count, st);
+}
+
+int phase3_impl(Workspace& ws, const hrb_slice* s, const SliceDev& sd, int split, const uint64_t* sub_keys,
+                const uint64_t* sub_count, uint64_t sub_cap, uint64_t* cm, uint64_t* cd, uint64_t* cdom,
+                uint64_t* cand_count, uint64_t cap, cudaStream_t st) {
+    int rc;
+    const uint64_t maxstep = s->max_dom_n;  // >= every subdomain step
+    const uint64_t CH = (maxstep + CHUNK3 - 1) / CHUNK3;
+    const uint64_t items = sub_cap * (CH ? CH : 1);
+    if ((rc = ws.counts3.ensure(sizeof(uint32_t) * (items + 1)))) return rc;
+    if ((rc = ws.offs3.ensure(sizeof(uint64_t) * (items + 1)))) return rc;
+    const uint64_t app_cap = cap;
+    if ((rc = ws.app.ensure(sizeof(Cand) * (app_cap + 1)))) return rc;
+    if ((rc = ws.appc.ensure(sizeof(unsigned long long)))) return rc;
+    CK(cudaMemsetAsync(ws.appc.p, 0, sizeof(unsigned long long), st));
+    const int grid = sm_count() * 8;
+    phase3_kernel<<<grid, 256, 0, st>>>(sd, split, sub_keys, sub_count, sub_cap, (const unsigned long long*)ws.meta.p,
+                                        (uint32_t*)ws.counts3.p, (Cand*)ws.app.p, (unsigned long long*)ws.appc.p,
+                                        app_cap);
+    CK(cudaGetLastError());
+    P3Offsets fn{(const uint32_t*)ws.counts3.p, sub_count, sub_cap, (const unsigned long long*)ws.meta.p,
+                 (uint64_t*)ws.offs3.p};
+    if ((rc = run_compact(ws, fn, cand_count, st))) return rc;
+    scatter3_kernel<<<sm_count() * 2, 256, 0, st>>>((const Cand*)ws.app.p, (const unsigned long long*)ws.appc.p,
+                                                    app_cap, (const uint64_t*)ws.offs3.p, cm, cd, cdom, cap);
+    CK(cudaGetLastError());
+    return HRB_OK;
+}
+
+int check_algo(int algo, int mode) {
+    if (algo < 0 || algo > 3) return set_err(HRB_ERR_CONFIG, "unknown algorithm code");
+    if (mode < 0 || mode > 2) return set_err(HRB_ERR_CONFIG, "unknown division mode code");
+    return HRB_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C-ABI
+// ===========================================================================
+extern "C" {
+
+int hrb_version(void) { return 100; }
+
+const char* hrb_last_error(void) { return g_err.c_str(); }
+
+int hrb_device_info(int device, char* buf, int buflen) {
+    cudaDeviceProp p;
+    CK(cudaGetDeviceProperties(&p, device));
+    int clk = 0;
+    cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, device);
+    snprintf(buf, (size_t)buflen, "%s sm_%d%d SMs=%d clock_khz=%d", p.name, p.major, p.minor, p.multiProcessorCount,
+             clk);
+    return HRB_OK;
+}
+
+int hrb_search_batch(int algo, int mode, int word_bits, int64_t n, const uint64_t* a, const uint64_t* b,
+                     const uint64_t* eps, const uint64_t* count, uint8_t* ok, uint64_t* d, uint64_t* iterations,
+                     uint64_t* points_lo, uint8_t* points_hi, void* stream) {
+    int rc = check_algo(algo, mode);
+    if (rc) return rc;
+    if (word_bits != 32 && word_bits != 64) return set_err(HRB_ERR_CONFIG, "word_bits must be 32 or 64");
+    if (n < 0) return set_err(HRB_ERR_CONFIG, "negative batch size");
+    if (n == 0) return HRB_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    int64_t blocks = (n + 255) / 256;
+    int cap = sm_count() * 16;
+    int grid = (int)(blocks < cap ? blocks : cap);
+    const bool reg = algo >= hrb::ALGO_REGULAR;
+#define SB(WV, RV) \
+    search_batch_kernel<WV, RV><<<grid, 256, 0, st>>>(algo, mode, n, a, b, eps, count, ok, d, iterations, points_lo, points_hi)
+    if (word_bits == 64 && reg) SB(64, true);
+    else if (word_bits == 64) SB(64, false);
+    else if (reg) SB(32, true);
+    else SB(32, false);
+#undef SB
+    CK(cudaGetLastError());
+    return HRB_OK;
+}
+
+int hrb_domain_coefficients(const hrb_slice* s, uint32_t* out, void* stream) {
+    int rc = check_slice(s);
+    if (rc) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    Workspace* ws;
+    if ((rc = current_ws(&ws))) return rc;
+    SliceDev sd = to_dev(s);
+    if ((rc = ws_prep(*ws, sd, 2, st))) return rc;
+    const int grid = sm_count() * 4;
+    const uint64_t* tb = (const uint64_t*)ws->tile_base.p;
+    const int64_t nt = s->n_total;
+    switch (s->coef_limbs) {
+#define CASE(CLV) \
+    case CLV: tabdiff_full_kernel<CLV><<<grid, 128, 0, st>>>(sd, tb, nt, out); break;
+        CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10) CASE(11) CASE(12)
+        CASE(13) CASE(14) CASE(15) CASE(16)
+#undef CASE
+        default: return set_err(HRB_ERR_CONFIG, "coef_limbs outside [1, 16]");
+    }
+    CK(cudaGetLastError());
+    return HRB_OK;
+}
+
+int hrb_phase1(const hrb_slice* s, int algo, int mode, uint64_t* fail_ids, uint64_t* fail_count, uint64_t cap,
+               uint64_t* iter_sum, void* stream) {
+    int rc = check_slice(s);
+    if (rc || (rc = check_algo(algo, mode))) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    Workspace* ws;
+    if ((rc = current_ws(&ws))) return rc;
+    SliceDev sd = to_dev(s);
+    if ((rc = ws_prep(*ws, sd, 2, st))) return rc;
+    return phase1_impl(*ws, s, sd, algo, mode, fail_ids, fail_count, cap, iter_sum, st);
+}
+
+int hrb_phase2(const hrb_slice* s, int algo, int mode, int split, const uint64_t* fail_ids,
+               const uint64_t* fail_count, uint64_t fail_cap, uint64_t* sub_keys, uint64_t* sub_count, uint64_t cap,
+               void* stream) {
+    int rc = check_slice(s);
+    if (rc || (rc = check_algo(algo, mode))) return rc;
+    if (split < 2 || split > 64) return set_err(HRB_ERR_CONFIG, "phase2_split outside {2..64}");
+    cudaStream_t st = (cudaStream_t)stream;
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    Workspace* ws;
+    if ((rc = current_ws(&ws))) return rc;
+    SliceDev sd = to_dev(s);
+    if ((rc = ws_prep(*ws, sd, split, st))) return rc;
+    return phase2_impl(*ws, s, sd, algo, mode, split, fail_ids, fail_count, fail_cap, sub_keys, sub_count, cap, st);
+}
+
+int hrb_phase3(const hrb_slice* s, int split, const uint64_t* sub_keys, const uint64_t* sub_count, uint64_t sub_cap,
+               uint64_t* cand_index, uint64_t* cand_dist, uint64_t* cand_dom, uint64_t* cand_count, uint64_t cap,
+               void* stream) {
+    int rc = check_slice(s);
+    if (rc) return rc;
+    if (split < 1 || split > 64) return set_err(HRB_ERR_CONFIG, "split outside {1..64}");
+    cudaStream_t st = (cudaStream_t)stream;
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    Workspace* ws;
+    if ((rc = current_ws(&ws))) return rc;
+    SliceDev sd = to_dev(s);
+    if ((rc = ws_prep(*ws, sd, split, st))) return rc;
+    return phase3_impl(*ws, s, sd, split, sub_keys, sub_count, sub_cap, cand_index, cand_dist, cand_dom, cand_count,
+                       cap, st);
+}
+
+int hrb_run_slice(const hrb_slice* s, int algo, int mode, int split, const hrb_run_out* out, void* stream) {
+    int rc = check_slice(s);
+    if (rc || (rc = check_algo(algo, mode))) return rc;
+    if (split < 2 || split > 64) return set_err(HRB_ERR_CONFIG, "phase2_split outside {2..64}");
+    cudaStream_t st = (cudaStream_t)stream;
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    Workspace* ws;
+    if ((rc = current_ws(&ws))) return rc;
+    SliceDev sd = to_dev(s);
+    uint64_t* counts = out->counts;
+    CK(cudaMemsetAsync(counts, 0, sizeof(uint64_t) * 4, st));
+    if ((rc = ws_prep(*ws, sd, split, st))) return rc;
+    if ((rc = phase1_impl(*ws, s, sd, algo, mode, out->fail_ids, counts + 0, out->fail_cap, counts + 3, st)))
+        return rc;
+    if ((rc = phase2_impl(*ws, s, sd, algo, mode, split, out->fail_ids, counts + 0, out->fail_cap, out->sub_keys,
+                          counts + 1, out->sub_cap, st)))
+        return rc;
+    return phase3_impl(*ws, s, sd, split, out->sub_keys, counts + 1, out->sub_cap, out->cand_index, out->cand_dist,
+                       out->cand_dom, counts + 2, out->cand_cap, st);
+}
+
+namespace {
+struct HostRunState {
+    Buf coef, G, s2, nd, dn, ln, db, m0, fail, sub, cm, cd, cdom, counts;
+    cudaStream_t st = nullptr;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+};
+HostRunState g_host[64];
+}  // namespace
+
+int hrb_run_slice_host(const hrb_slice* hs, int algo, int mode, int split, uint64_t* counts, uint64_t* fail_ids,
+                       uint64_t fail_cap, uint64_t* cand_index, uint64_t* cand_dist, uint64_t* cand_dom,
+                       uint64_t cand_cap, float* device_ms) {
+    int rc = check_slice(hs);
+    if (rc || (rc = check_algo(algo, mode))) return rc;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    HostRunState& H = g_host[dev & 63];
+    if (!H.st) {
+        CK(cudaStreamCreateWithFlags(&H.st, cudaStreamNonBlocking));
+        CK(cudaEventCreate(&H.e0));
+        CK(cudaEventCreate(&H.e1));
+    }
+    const int64_t S = hs->n_super, CL = hs->coef_limbs, NT = hs->n_total;
+    const size_t b_coef = sizeof(uint32_t) * 6 * CL * S, b2 = sizeof(uint64_t) * 2 * S, b32 = sizeof(uint32_t) * S;
+    if ((rc = H.coef.ensure(b_coef)) || (rc = H.G.ensure(b2)) || (rc = H.s2.ensure(b2)) || (rc = H.nd.ensure(b32)) ||
+        (rc = H.dn.ensure(b32)) || (rc = H.ln.ensure(b32)) || (rc = H.db.ensure(sizeof(uint64_t) * (S + 1))) ||
+        (rc = H.m0.ensure(sizeof(uint64_t) * S)) || (rc = H.counts.ensure(sizeof(uint64_t) * 4)))
+        return rc;
+    cudaStream_t st = H.st;
+    CK(cudaEventRecord(H.e0, st));
+    CK(cudaMemcpyAsync(H.coef.p, hs->coef, b_coef, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(H.G.p, hs->G, b2, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(H.s2.p, hs->s2abs, b2, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(H.nd.p, hs->n_dom, b32, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(H.dn.p, hs->dom_n, b32, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(H.ln.p, hs->last_n, b32, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(H.db.p, hs->dom_base, sizeof(uint64_t) * (S + 1), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(H.m0.p, hs->m0, sizeof(uint64_t) * S, cudaMemcpyHostToDevice, st));
+    hrb_slice ds = *hs;
+    ds.coef = (const uint32_t*)H.coef.p;
+    ds.G = (const uint64_t*)H.G.p;
+    ds.s2abs = (const uint64_t*)H.s2.p;
+    ds.n_dom = (const uint32_t*)H.nd.p;
+    ds.dom_n = (const uint32_t*)H.dn.p;
+    ds.last_n = (const uint32_t*)H.ln.p;
+    ds.dom_base = (const uint64_t*)H.db.p;
+    ds.m0 = (const uint64_t*)H.m0.p;
+    uint64_t sub_cap = (uint64_t)NT * 2 + 1024;
+    const uint64_t fcap = (uint64_t)NT;
+    for (int attempt = 0; attempt < 2; attempt++) {
+        if ((rc = H.fail.ensure(sizeof(uint64_t) * (fcap + 1))) || (rc = H.sub.ensure(sizeof(uint64_t) * (sub_cap + 1))) ||
+            (rc = H.cm.ensure(sizeof(uint64_t) * (cand_cap + 1))) ||
+            (rc = H.cd.ensure(sizeof(uint64_t) * (cand_cap + 1))) ||
+            (rc = H.cdom.ensure(sizeof(uint64_t) * (cand_cap + 1))))
+            return rc;
+        hrb_run_out o;
+        o.fail_ids = (uint64_t*)H.fail.p;
+        o.fail_cap = fcap;
+        o.sub_keys = (uint64_t*)H.sub.p;
+        o.sub_cap = sub_cap;
+        o.cand_index = (uint64_t*)H.cm.p;
+        o.cand_dist = (uint64_t*)H.cd.p;
+        o.cand_dom = (uint64_t*)H.cdom.p;
+        o.cand_cap = cand_cap;
+        o.counts = (uint64_t*)H.counts.p;
+        if ((rc = hrb_run_slice(&ds, algo, mode, split, &o, st))) return rc;
+        CK(cudaMemcpyAsync(counts, H.counts.p, sizeof(uint64_t) * 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (counts[1] <= sub_cap) break;
+        sub_cap = counts[1] + 1024;  // grow once and re-run
+        CK(cudaEventRecord(H.e0, st));
+    }
+    const uint64_t nf = counts[0] < fail_cap ? counts[0] : fail_cap;
+    const uint64_t nc = counts[2] < cand_cap ? counts[2] : cand_cap;
+    if (fail_ids && nf) CK(cudaMemcpyAsync(fail_ids, H.fail.p, sizeof(uint64_t) * nf, cudaMemcpyDeviceToHost, st));
+    if (nc) {
+        CK(cudaMemcpyAsync(cand_index, H.cm.p, sizeof(uint64_t) * nc, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(cand_dist, H.cd.p, sizeof(uint64_t) * nc, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(cand_dom, H.cdom.p, sizeof(uint64_t) * nc, cudaMemcpyDeviceToHost, st));
+    }
+    CK(cudaEventRecord(H.e1, st));
+    CK(cudaStreamSynchronize(st));
+    if (device_ms) CK(cudaEventElapsedTime(device_ms, H.e0, H.e1));
+    if (counts[0] > fail_cap && fail_ids) return set_err(HRB_ERR_CAPACITY, "fail_ids buffer too small");
+    if (counts[2] > cand_cap) return set_err(HRB_ERR_CAPACITY, "candidate buffer too small");
+    return HRB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,212 @@
+"""Device-side execution of a packed slice through libhrb200 (C-ABI).
+
+torch supplies device memory and the stream; every computation is a call
+into include/hrb200.h.  There is no CPU fallback (see _native.require_cuda).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as nat
+from .slices import SliceBatch
+
+
+def _t(torch, arr: np.ndarray, device):
+    return torch.from_numpy(np.ascontiguousarray(arr)).to(device, non_blocking=False)
+
+
+class DeviceSlice:
+    """A SliceBatch resident in HBM plus its hrb_slice descriptor."""
+
+    def __init__(self, batch: SliceBatch, device=None):
+        torch = nat.require_cuda()
+        self.torch = torch
+        self.batch = batch
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        u32 = lambda a: _t(torch, a.view(np.int32), self.device)  # noqa: E731  (torch lacks uint32 ops)
+        u64 = lambda a: _t(torch, a.view(np.int64), self.device)  # noqa: E731
+        self.coef = u32(batch.coef)
+        self.G = u64(batch.G)
+        self.s2abs = u64(batch.s2abs)
+        self.n_dom = u32(batch.n_dom)
+        self.dom_n = u32(batch.dom_n)
+        self.last_n = u32(batch.last_n)
+        self.dom_base = u64(batch.dom_base)
+        self.m0 = u64(batch.m0)
+        self.desc = nat.HrbSlice(
+            n_super=batch.n_super, n_total=batch.n_total, max_dom_n=batch.max_dom_n,
+            coef_limbs=batch.coef_limbs, frac_bits=batch.frac_bits, word_bits=batch.word_bits, delta=batch.delta,
+            coef=self.coef.data_ptr(), G=self.G.data_ptr(), s2abs=self.s2abs.data_ptr(),
+            n_dom=self.n_dom.data_ptr(), dom_n=self.dom_n.data_ptr(), last_n=self.last_n.data_ptr(),
+            dom_base=self.dom_base.data_ptr(), m0=self.m0.data_ptr())
+
+    def empty64(self, n: int):
+        return self.torch.empty(max(int(n), 1), dtype=self.torch.int64, device=self.device)
+
+
+@dataclass
+class SliceResult:
+    """Device outputs of one slice, on the host (slice-local ids)."""
+
+    fail_ids: np.ndarray      # uint64, ascending
+    sub_keys: np.ndarray      # uint64 (local id << 8 | j), ascending
+    cand_index: np.ndarray    # uint64 binade argument index, ascending
+    cand_dist: np.ndarray     # uint64 distance floored to 2^-64
+    cand_dom: np.ndarray      # uint64 slice-local domain id
+    iterations: int           # phase-1 SearchOutcome.iterations sum
+    phase_ms: tuple = (0.0, 0.0, 0.0)
+
+
+def _u64(t) -> np.ndarray:
+    return t.cpu().numpy().view(np.uint64)
+
+
+def run_phases(ds: DeviceSlice, algo_code: int, mode_code: int, split: int, cand_hint: int = 4096,
+               timed: bool = True) -> SliceResult:
+    """Phase 1, 2, 3 as separate ABI calls with the counts read back between
+    them (sizes the next phase's buffers; wall times per phase like the
+    reference's PhaseRow)."""
+    torch = ds.torch
+    lib = nat.load()
+    b = ds.batch
+    st = nat.stream_ptr()
+    stream = torch.cuda.current_stream()
+    n_total = b.n_total
+    cnt = ds.empty64(4)
+    cnt.zero_()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    # phase 1
+    fail = ds.empty64(n_total)
+    ev[0].record(stream)
+    nat.check("hrb_phase1", lib.hrb_phase1(C.byref(ds.desc), algo_code, mode_code, fail.data_ptr(),
+                                           cnt.data_ptr(), n_total, cnt[3:].data_ptr(), st))
+    ev[1].record(stream)
+    n_fail = int(cnt[0].item())
+    # phase 2
+    jmax = 2 * split
+    sub_cap = max(n_fail * jmax, 1)
+    subs = ds.empty64(sub_cap)
+    nat.check("hrb_phase2", lib.hrb_phase2(C.byref(ds.desc), algo_code, mode_code, split, fail.data_ptr(),
+                                           cnt[0:].data_ptr(), n_total, subs.data_ptr(), cnt[1:].data_ptr(),
+                                           sub_cap, st))
+    ev[2].record(stream)
+    n_sub = int(cnt[1].item())
+    # phase 3 (grow the candidate buffer once if the hint was too small)
+    cap = max(cand_hint, 1)
+    while True:
+        cm, cdist, cdom = ds.empty64(cap), ds.empty64(cap), ds.empty64(cap)
+        nat.check("hrb_phase3", lib.hrb_phase3(C.byref(ds.desc), split, subs.data_ptr(), cnt[1:].data_ptr(),
+                                               sub_cap, cm.data_ptr(), cdist.data_ptr(), cdom.data_ptr(),
+                                               cnt[2:].data_ptr(), cap, st))
+        n_c = int(cnt[2].item())
+        if n_c <= cap:
+            break
+        cap = n_c
+    ev[3].record(stream)
+    torch.cuda.synchronize()
+    ms = tuple(ev[k].elapsed_time(ev[k + 1]) for k in range(3)) if timed else (0.0, 0.0, 0.0)
+    return SliceResult(_u64(fail[:n_fail]), _u64(subs[:n_sub]), _u64(cm[:n_c]), _u64(cdist[:n_c]),
+                       _u64(cdom[:n_c]), int(cnt[3].item()), ms)
+
+
+class FusedRunner:
+    """hrb_run_slice with persistent device buffers: the bench hot path
+    (inputs resident in HBM, no host synchronisation inside a step)."""
+
+    def __init__(self, ds: DeviceSlice, algo_code: int, mode_code: int, split: int, sub_cap: int,
+                 cand_cap: int):
+        self.ds = ds
+        self.algo, self.mode, self.split = algo_code, mode_code, split
+        n_total = ds.batch.n_total
+        self.fail = ds.empty64(n_total)
+        self.subs = ds.empty64(sub_cap)
+        self.cm, self.cd, self.cdom = ds.empty64(cand_cap), ds.empty64(cand_cap), ds.empty64(cand_cap)
+        self.counts = ds.empty64(4)
+        self.out = nat.HrbRunOut(fail_ids=self.fail.data_ptr(), fail_cap=n_total, sub_keys=self.subs.data_ptr(),
+                                 sub_cap=sub_cap, cand_index=self.cm.data_ptr(), cand_dist=self.cd.data_ptr(),
+                                 cand_dom=self.cdom.data_ptr(), cand_cap=cand_cap, counts=self.counts.data_ptr())
+        self.sub_cap, self.cand_cap = sub_cap, cand_cap
+
+    def launch(self, stream=None) -> None:
+        lib = nat.load()
+        nat.check("hrb_run_slice", lib.hrb_run_slice(C.byref(self.ds.desc), self.algo, self.mode, self.split,
+                                                     C.byref(self.out), nat.stream_ptr(stream)))
+
+    def counts_host(self) -> np.ndarray:
+        return self.counts.cpu().numpy().view(np.uint64)
+
+    def result(self) -> SliceResult:
+        c = self.counts_host()
+        if c[1] > self.sub_cap or c[2] > self.cand_cap:
+            raise nat.NativeError("hrb_run_slice", nat.HRB_ERR_CAPACITY, f"counts {c.tolist()} exceed capacity")
+        nf, ns, nc = int(c[0]), int(c[1]), int(c[2])
+        return SliceResult(_u64(self.fail[:nf]), _u64(self.subs[:ns]), _u64(self.cm[:nc]), _u64(self.cd[:nc]),
+                           _u64(self.cdom[:nc]), int(c[3]))
+
+
+def run_host(batch: SliceBatch, algo_code: int, mode_code: int, split: int, cand_cap: int = 1 << 16):
+    """hrb_run_slice_host: host buffers in, host results out (the e2e path).
+    Returns (counts, fail_ids, cand_index, cand_dist, cand_dom, device_ms)."""
+    nat.require_cuda()
+    lib = nat.load()
+    arrs = [np.ascontiguousarray(a) for a in (batch.coef, batch.G, batch.s2abs, batch.n_dom, batch.dom_n,
+                                               batch.last_n, batch.dom_base, batch.m0)]
+    p = [a.ctypes.data for a in arrs]
+    desc = nat.HrbSlice(n_super=batch.n_super, n_total=batch.n_total, max_dom_n=batch.max_dom_n,
+                        coef_limbs=batch.coef_limbs, frac_bits=batch.frac_bits, word_bits=batch.word_bits,
+                        delta=batch.delta, coef=p[0], G=p[1], s2abs=p[2], n_dom=p[3], dom_n=p[4], last_n=p[5],
+                        dom_base=p[6], m0=p[7])
+    counts = np.zeros(4, dtype=np.uint64)
+    fail = np.zeros(max(batch.n_total, 1), dtype=np.uint64)
+    while True:
+        cm = np.zeros(cand_cap, dtype=np.uint64)
+        cd = np.zeros(cand_cap, dtype=np.uint64)
+        cdom = np.zeros(cand_cap, dtype=np.uint64)
+        ms = C.c_float(0)
+        rc = lib.hrb_run_slice_host(C.byref(desc), algo_code, mode_code, split, counts.ctypes.data, fail.ctypes.data,
+                                    fail.size, cm.ctypes.data, cd.ctypes.data, cdom.ctypes.data, cand_cap,
+                                    C.byref(ms))
+        if rc == nat.HRB_ERR_CAPACITY and counts[2] > cand_cap:
+            cand_cap = int(counts[2])
+            continue
+        nat.check("hrb_run_slice_host", rc)
+        break
+    nf, nc = int(counts[0]), int(counts[2])
+    return counts, fail[:nf], cm[:nc], cd[:nc], cdom[:nc], ms.value
+
+
+def domain_coefficients(ds: DeviceSlice) -> np.ndarray:
+    """hrb_domain_coefficients -> uint32 [3, CL, n_total] (two's complement)."""
+    torch = ds.torch
+    lib = nat.load()
+    b = ds.batch
+    out = torch.empty(3 * b.coef_limbs * max(b.n_total, 1), dtype=torch.int32, device=ds.device)
+    nat.check("hrb_domain_coefficients", lib.hrb_domain_coefficients(C.byref(ds.desc), out.data_ptr(),
+                                                                     nat.stream_ptr()))
+    torch.cuda.synchronize()
+    return out.cpu().numpy().view(np.uint32).reshape(3, b.coef_limbs, -1)[:, :, : b.n_total]
+
+
+def search_batch_arrays(algo_code: int, mode_code: int, word_bits: int, a, b, eps, count, device=None):
+    """hrb_search_batch over host arrays; returns host arrays
+    (ok, d, iterations, points_lo, points_hi)."""
+    torch = nat.require_cuda()
+    lib = nat.load()
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    n = len(a)
+    ins = [torch.from_numpy(np.ascontiguousarray(np.asarray(x, dtype=np.uint64)).view(np.int64)).to(dev)
+           for x in (a, b, eps, count)]
+    ok = torch.empty(max(n, 1), dtype=torch.uint8, device=dev)
+    d = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+    it = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+    pl = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+    ph = torch.empty(max(n, 1), dtype=torch.uint8, device=dev)
+    nat.check("hrb_search_batch", lib.hrb_search_batch(algo_code, mode_code, word_bits, n, *(x.data_ptr() for x in ins),
+                                                       ok.data_ptr(), d.data_ptr(), it.data_ptr(), pl.data_ptr(),
+                                                       ph.data_ptr(), nat.stream_ptr()))
+    torch.cuda.synchronize()
+    return (ok[:n].cpu().numpy(), _u64(d[:n]), _u64(it[:n]), _u64(pl[:n]), ph[:n].cpu().numpy())

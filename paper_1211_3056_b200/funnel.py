@@ -1,0 +1,356 @@
+"""Three-phase HR-case funnel with the phases on the GPU.
+
+Drop-in for /root/reference/pkg/src/hardround/pipeline.py: the same config
+types (PhaseConfig 48-69, PipelineConfig 72-86), statistics (PhaseRow /
+PhaseStats 89-112), task types (DomainTask / SubdomainTask 115-134),
+algorithm auto-selection (select_algorithm 187-197), the per-phase entry
+points (phase1 213-231, phase2 234-257, phase3_exhaustive 260-293) and the
+binade driver (run_pipeline 412-463).  `run_slice` is the same driver over
+an argument-index range (the reference runs only whole binades).
+
+Host: output-exponent pieces, Taylor models, hierarchical split and the
+final rigorous confirmation (decide_hr).  Device (include/hrb200.h): the
+tabulated coefficient walk, Boolean problems, both search families,
+subdomain refinement, the exhaustive walk, and all compaction.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+from fractions import Fraction
+from typing import Sequence
+
+import numpy as np
+
+from . import _native as nat
+from .arith import LIMB_BITS, MODE_CODE, DivisionMode, MPInt, UFrac, as_int
+from .enclosure import decide_hr
+from .fpformat import Domain, ErrorBudget, FpFormat, HrCaseRecord, bits_float, index_bits
+from .search import ALGO_CODE, Algorithm
+from .slices import (SliceBatch, SuperDomain, build_super_domains, check_phase2_exact, domain_poly,
+                     output_binade_pieces, pack_slice)
+from .taylor import BinomialPoly, PolyGenConfig, straightforward_shift
+
+ALGORITHMS = ("lefevre", "regular", "auto")
+SELECT_THRESHOLD = 1e-3
+
+
+@dataclass(frozen=True, slots=True)
+class PhaseConfig:
+    algorithm: str = "auto"
+    div_mode: DivisionMode = DivisionMode.HYBRID
+    phase2_split: int = 8
+    budgets: ErrorBudget | None = None
+    N1: int = 1 << 6
+    parallel_width: int = 1  # host workers for Taylor generation (the device needs none)
+
+    def __post_init__(self) -> None:
+        if self.algorithm not in ALGORITHMS:
+            raise ValueError(f"algorithm must be one of {ALGORITHMS}")
+        if not 2 <= self.phase2_split <= 64:
+            raise ValueError("phase2_split outside {2..64}")
+        if self.N1 % self.phase2_split:
+            raise ValueError("phase2_split must divide N1")
+        if not 1 <= self.parallel_width <= 64:
+            raise ValueError("parallel_width outside [1, 64]")
+
+
+@dataclass(frozen=True, slots=True)
+class PipelineConfig:
+    fn: str
+    fmt: FpFormat
+    polygen: PolyGenConfig = PolyGenConfig()
+    phase: PhaseConfig = PhaseConfig()
+    word_bits: int = 64
+
+    def __post_init__(self) -> None:
+        if self.phase.N1 != self.polygen.N:
+            raise ValueError("phase N1 and polygen N must agree")
+        if self.word_bits not in (32, 64):
+            raise ValueError("word_bits must be 32 or 64")
+        if self.polygen.frac_bits > self.polygen.limbs * LIMB_BITS:
+            raise ValueError("difference registers would not fit the limb budget")
+
+
+@dataclass(frozen=True, slots=True)
+class PhaseRow:
+    phase: str
+    domains_in: int
+    domains_out: int
+    arguments_covered: int
+    wall_ms: float
+
+
+@dataclass(slots=True)
+class PhaseStats:
+    rows: list = field(default_factory=list)
+    algorithm_choices: list = field(default_factory=list)
+
+    def row(self, phase: str) -> PhaseRow:
+        for r in self.rows:
+            if r.phase == phase:
+                return r
+        raise KeyError(phase)
+
+    def phase3_phase1_ratio(self) -> float:
+        p1 = self.row("phase1").domains_in
+        return self.row("phase3").domains_in / p1 if p1 else 0.0
+
+
+@dataclass(frozen=True, slots=True)
+class DomainTask:
+    domain: Domain
+    coeffs: tuple
+    frac_bits: int
+    eps_prime: Fraction
+    e_out: int
+
+
+@dataclass(frozen=True, slots=True)
+class SubdomainTask:
+    parent: DomainTask
+    sub_index: int
+    start: int
+    count: int
+    coeffs: tuple
+
+
+def select_algorithm(prev_interval_stats: PhaseStats | None, threshold: float = SELECT_THRESHOLD) -> str:
+    """Heavy funnels (phase3/phase1 > threshold) pick the classic walk."""
+    if prev_interval_stats is None:
+        return "regular"
+    try:
+        ratio = prev_interval_stats.phase3_phase1_ratio()
+    except KeyError:
+        return "regular"
+    return "lefevre" if ratio > threshold else "regular"
+
+
+def _resolve(cfg: PipelineConfig, algo: str | None) -> str:
+    return algo or (cfg.phase.algorithm if cfg.phase.algorithm != "auto" else "regular")
+
+
+# ------------------------------------------------------------------ slices
+
+
+@dataclass
+class SliceOutput:
+    """Everything one slice produced, in the reference's types and order."""
+
+    batch: SliceBatch
+    failing_ids: list          # phase-1 failing global domain ids (ascending)
+    sub_rows: list             # (parent id, sub index, start, count) ascending
+    candidates: list           # HrCaseRecord candidates of phase 3 (argument order)
+    records: list              # confirmed HR records (sorted)
+    stats: PhaseStats
+    iterations: int            # phase-1 quotient steps (SearchOutcome.iterations)
+
+
+def _sub_geometry(n: np.ndarray, j: np.ndarray, split: int):
+    step = np.maximum(n // np.uint64(split), np.uint64(1))
+    start = j * step
+    cnt = np.minimum(step, n - start)
+    return start, cnt
+
+
+def execute_batch(batch: SliceBatch, cfg: PipelineConfig, algo: str, fn: str | None = None,
+                  confirm: bool = True) -> SliceOutput:
+    """Run phases 1-3 of a packed slice on the current CUDA device, then
+    confirm the candidates on the host (pipeline.py:447-462)."""
+    from .device import DeviceSlice, run_phases
+
+    fmt = cfg.fmt
+    split = cfg.phase.phase2_split
+    ds = DeviceSlice(batch)
+    res = run_phases(ds, ALGO_CODE[Algorithm(algo)], MODE_CODE[cfg.phase.div_mode], split)
+    id0 = batch.id0
+    # phase-2 MPInt replay for blocks whose shift bound was inconclusive
+    if batch.shift_bound_ok is not None and not batch.shift_bound_ok.all():
+        t_idx, i_idx = batch.locate(res.fail_ids)
+        for t, i in zip(t_idx.tolist(), i_idx.tolist()):
+            if not batch.shift_bound_ok[t]:
+                check_phase2_exact(batch.supers[t], i, split, cfg.polygen.limbs)
+    stats = PhaseStats()
+    fail_sizes = batch.domain_sizes(res.fail_ids)
+    stats.rows.append(PhaseRow("phase1", batch.n_total, len(res.fail_ids), batch.arguments, res.phase_ms[0]))
+    sub_local = res.sub_keys >> np.uint64(8)
+    sub_j = res.sub_keys & np.uint64(255)
+    sub_n = batch.domain_sizes(sub_local)
+    sub_start, sub_cnt = _sub_geometry(sub_n, sub_j, split)
+    stats.rows.append(PhaseRow("phase2", len(res.fail_ids), len(res.sub_keys), int(fail_sizes.sum()),
+                               res.phase_ms[1]))
+    cand = [HrCaseRecord(index_bits(batch.binade, int(m), fmt), UFrac(int(dd), 64), id0 + int(dm))
+            for m, dd, dm in zip(res.cand_index.tolist(), res.cand_dist.tolist(), res.cand_dom.tolist())]
+    stats.rows.append(PhaseRow("phase3", len(res.sub_keys), len(cand), int(sub_cnt.sum()), res.phase_ms[2]))
+    records = []
+    t4 = time.perf_counter()
+    if confirm:
+        fn = fn or cfg.fn
+        guard = 2 * (fmt.precision + fmt.eps_bits) + 16
+        for c in cand:
+            dec = decide_hr(fn, bits_float(c.argument, fmt), fmt, start_prec=guard)
+            if dec.is_hr:
+                records.append(HrCaseRecord(c.argument, UFrac.from_fraction(dec.distance_lo), c.domain_id))
+        records.sort()
+    stats.rows.append(PhaseRow("confirm", len(cand), len(records), len(cand), (time.perf_counter() - t4) * 1e3))
+    rows = list(zip((id0 + sub_local).tolist(), sub_j.tolist(), sub_start.tolist(), sub_cnt.tolist()))
+    return SliceOutput(batch, [id0 + int(x) for x in res.fail_ids.tolist()], rows, cand, records, stats,
+                       res.iterations)
+
+
+def prepare_slice(fn: str, binade: int, start: int, count: int, cfg: PipelineConfig, workers: int | None = None,
+                  id0: int = 0) -> SliceBatch:
+    """Host half: Taylor blocks of the range, packed and checked."""
+    w = workers if workers is not None else cfg.phase.parallel_width
+    supers = build_super_domains(fn, binade, cfg.fmt, cfg.polygen, start, count, workers=w, id0=id0)
+    ceiling = cfg.phase.budgets.eps_dprime if cfg.phase.budgets is not None else None
+    return pack_slice(supers, cfg.fmt, cfg.polygen, cfg.word_bits, binade, budget_ceiling=ceiling)
+
+
+def run_slice(fn: str, binade: int, start: int, count: int, cfg: PipelineConfig, algo: str | None = None,
+              workers: int | None = None) -> SliceOutput:
+    """The funnel over argument indices [start, start+count) of one binade."""
+    batch = prepare_slice(fn, binade, start, count, cfg, workers)
+    return execute_batch(batch, cfg, _resolve(cfg, algo), fn)
+
+
+def run_pipeline(binade: int, cfg: PipelineConfig, prev_stats: PhaseStats | None = None):
+    """Full funnel over one binade -> (records ascending, PhaseStats)."""
+    algo = cfg.phase.algorithm
+    if algo == "auto":
+        algo = select_algorithm(prev_stats)
+    out = run_slice(cfg.fn, binade, 0, 1 << (cfg.fmt.precision - 1), cfg, algo)
+    out.stats.algorithm_choices.append((binade, algo))
+    return out.records, out.stats
+
+
+# --------------------------------------------------- per-phase drop-ins
+
+
+def _task_slice(items, cfg: PipelineConfig, binade: int) -> SliceBatch:
+    """Pack explicit (coeffs, count, eps', index) items as one-domain
+    super-domains: r_0 = (s0, 0, 0), r_1 = (s1, 0), r_2 = (s2,).  A missing
+    s2 (delta = 1) packs as 0, which is exactly the reference's
+    len(coeffs) < 3 truncation rule (pipeline.py:144-145)."""
+    supers = []
+    for k, (coeffs, count, eps_prime, index) in enumerate(items):
+        c = [as_int(x) for x in coeffs] + [0] * (3 - len(coeffs))
+        rp = (BinomialPoly((c[0], 0, 0)), BinomialPoly((c[1], 0)), BinomialPoly((c[2],)))
+        supers.append(SuperDomain(index, count, count, 1, 1, 1, 0, k, rp, eps_prime))
+    pg = cfg.polygen
+    one = PolyGenConfig(tau=1, N=1, mu=1, nu=1, delta=2, limbs=pg.limbs, frac_bits=pg.frac_bits, guard=pg.guard)
+    ceiling = cfg.phase.budgets.eps_dprime if cfg.phase.budgets is not None else None
+    return pack_slice(supers, cfg.fmt, one, cfg.word_bits, binade, budget_ceiling=ceiling)
+
+
+def _binade_of(dom: Domain, fmt: FpFormat) -> int:
+    return dom.exponent - 1
+
+
+def phase1(tasks: Sequence[DomainTask], cfg: PipelineConfig, algo: str | None = None) -> list[int]:
+    """Failing domain ids of explicit DomainTasks (one device launch)."""
+    tasks = list(tasks)
+    if not tasks:
+        return []
+    from .device import DeviceSlice, run_phases
+
+    m_base = 1 << (cfg.fmt.precision - 1)
+    batch = _task_slice([(t.coeffs, t.domain.count, t.eps_prime, t.domain.m_start - m_base) for t in tasks], cfg,
+                        _binade_of(tasks[0].domain, cfg.fmt))
+    res = _phase1_only(batch, cfg, _resolve(cfg, algo))
+    return [tasks[int(i)].domain.domain_id for i in res]
+
+
+def _phase1_only(batch: SliceBatch, cfg: PipelineConfig, algo: str) -> np.ndarray:
+    import ctypes as C
+
+    from .device import DeviceSlice
+
+    ds = DeviceSlice(batch)
+    lib = nat.load()
+    fail = ds.empty64(batch.n_total)
+    cnt = ds.empty64(4)
+    cnt.zero_()
+    nat.check("hrb_phase1", lib.hrb_phase1(C.byref(ds.desc), ALGO_CODE[Algorithm(algo)], MODE_CODE[cfg.phase.div_mode],
+                                           fail.data_ptr(), cnt.data_ptr(), batch.n_total, None, nat.stream_ptr()))
+    n = int(cnt[0].item())
+    return fail[:n].cpu().numpy().view(np.uint64)
+
+
+def phase2(tasks: Sequence[DomainTask], cfg: PipelineConfig, algo: str | None = None) -> list[SubdomainTask]:
+    """Split each task s ways, shift, re-test; survivors in task order."""
+    tasks = list(tasks)
+    if not tasks:
+        return []
+    import ctypes as C
+
+    from .device import DeviceSlice
+
+    m_base = 1 << (cfg.fmt.precision - 1)
+    batch = _task_slice([(t.coeffs, t.domain.count, t.eps_prime, t.domain.m_start - m_base) for t in tasks], cfg,
+                        _binade_of(tasks[0].domain, cfg.fmt))
+    split = cfg.phase.phase2_split
+    ds = DeviceSlice(batch)
+    lib = nat.load()
+    torch = ds.torch
+    ids = torch.arange(len(tasks), dtype=torch.int64, device=ds.device)
+    cnt = ds.empty64(4)
+    cnt.zero_()
+    cnt[0] = len(tasks)
+    cap = len(tasks) * 2 * split
+    subs = ds.empty64(cap)
+    nat.check("hrb_phase2", lib.hrb_phase2(C.byref(ds.desc), ALGO_CODE[Algorithm(_resolve(cfg, algo))],
+                                           MODE_CODE[cfg.phase.div_mode], split, ids.data_ptr(), cnt.data_ptr(),
+                                           len(tasks), subs.data_ptr(), cnt[1:].data_ptr(), cap, nat.stream_ptr()))
+    n = int(cnt[1].item())
+    keys = subs[:n].cpu().numpy().view(np.uint64)
+    out = []
+    for key in keys.tolist():
+        t, j = key >> 8, key & 255
+        task = tasks[t]
+        n_t = task.domain.count
+        step = max(n_t // split, 1)
+        start = j * step
+        cnt_j = min(step, n_t - start)
+        poly = BinomialPoly(tuple(task.coeffs), task.frac_bits)
+        out.append(SubdomainTask(task, j, start, cnt_j, straightforward_shift(poly, start).coeffs))
+    return out
+
+
+def phase3_exhaustive(tasks: Sequence[SubdomainTask], cfg: PipelineConfig) -> list[HrCaseRecord]:
+    """Window test of every argument of the subdomains (device walk)."""
+    tasks = list(tasks)
+    if not tasks:
+        return []
+    import ctypes as C
+
+    from .device import DeviceSlice
+
+    fmt = cfg.fmt
+    m_base = 1 << (fmt.precision - 1)
+    binade = _binade_of(tasks[0].parent.domain, fmt)
+    batch = _task_slice([(s.coeffs, s.count, s.parent.eps_prime, s.parent.domain.m_start - m_base + s.start)
+                         for s in tasks], cfg, binade)
+    ds = DeviceSlice(batch)
+    lib = nat.load()
+    torch = ds.torch
+    keys = torch.arange(len(tasks), dtype=torch.int64, device=ds.device) << 8
+    cnt = ds.empty64(4)
+    cnt.zero_()
+    cnt[1] = len(tasks)
+    cap = 1 << 12
+    while True:
+        cm, cd, cdom = ds.empty64(cap), ds.empty64(cap), ds.empty64(cap)
+        nat.check("hrb_phase3", lib.hrb_phase3(C.byref(ds.desc), 1, keys.data_ptr(), cnt[1:].data_ptr(), len(tasks),
+                                               cm.data_ptr(), cd.data_ptr(), cdom.data_ptr(), cnt[2:].data_ptr(), cap,
+                                               nat.stream_ptr()))
+        n = int(cnt[2].item())
+        if n <= cap:
+            break
+        cap = n
+    m = cm[:n].cpu().numpy().view(np.uint64).tolist()
+    d = cd[:n].cpu().numpy().view(np.uint64).tolist()
+    dom = cdom[:n].cpu().numpy().view(np.uint64).tolist()
+    return [HrCaseRecord(index_bits(binade, mi, fmt), UFrac(di, 64), tasks[ti].parent.domain.domain_id)
+            for mi, di, ti in zip(m, d, dom)]

@@ -1,0 +1,364 @@
+"""Super-domain generation and packing into the device slice layout.
+
+Host half of the hybrid split (PAPER.md "CPU-GPU" polynomial generation):
+for an argument-index range of one binade this module reproduces the
+super-domain schedule of /root/reference/pkg/src/hardround/pipeline.py:374-409
+(_build_tasks: output-exponent pieces 296-347, adaptive domain size 350-371,
+tau*N blocks, taylor_approx + hierarchical_split per block), then packs the
+per-block r_j polynomials, the eps' budget and the domain geometry into the
+structure-of-arrays layout of include/hrb200.h (hrb_slice).
+
+It also performs every check that makes the reference raise on this path --
+MPInt limb overflow in the coefficient walk (fixedpoint.py:136), the eps''
+< 1/4 budget (fpmodel.py:224-225), the configured budget ceiling
+(pipeline.py:225-226) and the SearchProblem eps < 1/2 rule
+(lowerbound.py:64-65) -- exactly, so the device never sees a slice the
+reference would have rejected.
+"""
+
+from __future__ import annotations
+
+import math
+import os
+from dataclasses import dataclass, field
+from fractions import Fraction
+from typing import Sequence
+
+import numpy as np
+
+from .arith import LIMB_BITS, MPInt, MPOverflowError, as_int
+from .enclosure import derivative_bound, is_polynomial, value_exponent
+from .fpformat import Domain, ErrorBudget, FpFormat
+from .taylor import BinomialPoly, PolyGenConfig, hierarchical_split, straightforward_shift, taylor_approx
+
+
+@dataclass(frozen=True, slots=True)
+class SuperDomain:
+    """One Taylor block: `tau` domains of `n_p` arguments (the last may be
+    shorter) starting at binade index `index_start`."""
+
+    index_start: int
+    count: int
+    n_p: int
+    tau: int
+    mu: int
+    nu: int
+    e_out: int
+    dom_id0: int
+    r_polys: tuple          # BinomialPoly per j = 0..delta (hierarchical_split)
+    eps_prime: Fraction     # eps + eps_approx of this block
+
+    @property
+    def last_count(self) -> int:
+        return self.count - (self.tau - 1) * self.n_p
+
+    def domain_count(self, i: int) -> int:
+        return self.last_count if i == self.tau - 1 else self.n_p
+
+
+# ---------------------------------------------------------------- schedule
+
+
+def output_binade_pieces(fn: str, binade: int, fmt: FpFormat) -> list[tuple[int, int, int]]:
+    """Maximal runs (start, count, e_out) of constant output exponent over
+    the binade's argument indices (pipeline.py:296-347)."""
+    count = 1 << (fmt.precision - 1)
+    base = Domain(1 << (fmt.precision - 1), binade + 1, count)
+
+    def e_at(i: int) -> int:
+        return value_exponent(fn, base.x_at(i, fmt))
+
+    if is_polynomial(fn):
+        pieces, run_start, run_e = [], None, None
+        for i in range(count):
+            try:
+                e_i = e_at(i)
+            except ValueError:  # fn(x) == 0
+                e_i = None
+            if e_i != run_e:
+                if run_e is not None:
+                    pieces.append((run_start, i - run_start, run_e))
+                run_start, run_e = i, e_i
+        if run_e is not None:
+            pieces.append((run_start, count - run_start, run_e))
+        return pieces
+    start = 1 if (fn == "log" and binade == 0) else 0
+    pieces = []
+    while start < count:
+        e0 = e_at(start)
+        if e_at(count - 1) == e0:
+            pieces.append((start, count - start, e0))
+            break
+        lo, hi = start, count - 1  # e is monotone: binary search the last index with e0
+        while lo < hi:
+            mid = (lo + hi + 1) // 2
+            if e_at(mid) == e0:
+                lo = mid
+            else:
+                hi = mid - 1
+        pieces.append((start, lo - start + 1, e0))
+        start = lo + 1
+    return pieces
+
+
+def piece_domain_size(fn: str, piece: Domain, e_out: int, fmt: FpFormat, n_max: int) -> int:
+    """Largest power of two N <= n_max with |c2| (N-1)^2 < 1/8 on the piece
+    (pipeline.py:350-371)."""
+    norm = Fraction(2) ** (fmt.precision - e_out)
+    ulp = Fraction(2) ** (piece.exponent - fmt.precision)
+    c2 = norm * ulp**2 * derivative_bound(fn, 2, piece.x_at(0, fmt), piece.x_at(piece.count - 1, fmt))
+    n = n_max
+    while n > 1 and c2 * (n - 1) ** 2 >= Fraction(1, 8):
+        n //= 2
+    return n
+
+
+@dataclass(frozen=True, slots=True)
+class _Block:
+    fn: str
+    binade: int
+    fmt: FpFormat
+    bcfg: PolyGenConfig
+    bstart: int
+    bcount: int
+    n_p: int
+    e_out: int
+    dom_id0: int
+
+
+def _make_super(b: _Block) -> SuperDomain:
+    m_base = 1 << (b.fmt.precision - 1)
+    sup = Domain(m_base + b.bstart, b.binade + 1, b.bcount, b.dom_id0)
+    r_t, eps_approx = taylor_approx(b.fn, sup, b.bcfg, b.fmt)
+    r_polys = hierarchical_split(r_t, b.n_p, b.bcfg.delta)
+    return SuperDomain(b.bstart, b.bcount, b.n_p, b.bcfg.tau, b.bcfg.mu, b.bcfg.nu, b.e_out, b.dom_id0,
+                       tuple(r_polys), b.fmt.eps + eps_approx)
+
+
+def plan_blocks(fn: str, binade: int, fmt: FpFormat, pg: PolyGenConfig, start: int, count: int,
+                id0: int = 0) -> list[_Block]:
+    """The super-domain schedule of _build_tasks restricted to indices
+    [start, start + count); with the whole binade it is _build_tasks'."""
+    blocks, next_id = [], id0
+    for p_start, p_count, e_out in output_binade_pieces(fn, binade, fmt):
+        lo, hi = max(p_start, start), min(p_start + p_count, start + count)
+        if lo >= hi:
+            continue
+        piece = Domain((1 << (fmt.precision - 1)) + lo, binade + 1, hi - lo, 0)
+        n_p = piece_domain_size(fn, piece, e_out, fmt, pg.N)
+        block = pg.tau * n_p
+        for bstart in range(lo, hi, block):
+            bcount = min(block, hi - bstart)
+            if bcount == block and n_p == pg.N:
+                bcfg = pg
+            else:
+                tau_t = -(-bcount // n_p)
+                bcfg = PolyGenConfig(tau=tau_t, N=n_p, mu=1, nu=tau_t, delta=pg.delta,
+                                     limbs=pg.limbs, frac_bits=pg.frac_bits, guard=pg.guard)
+            blocks.append(_Block(fn, binade, fmt, bcfg, bstart, bcount, n_p, e_out, next_id))
+            next_id += bcfg.tau
+    return blocks
+
+
+def build_super_domains(fn: str, binade: int, fmt: FpFormat, pg: PolyGenConfig, start: int = 0,
+                        count: int | None = None, workers: int = 1, id0: int = 0) -> list[SuperDomain]:
+    """taylor_approx + hierarchical_split for every block of the range.
+    workers > 1 fans the (independent) blocks out to a process pool: the
+    mpmath host work, not the GPU, bounds large slices."""
+    if count is None:
+        count = (1 << (fmt.precision - 1)) - start
+    blocks = plan_blocks(fn, binade, fmt, pg, start, count, id0)
+    if workers > 1 and len(blocks) > 1:
+        import multiprocessing as mp
+
+        ctx = mp.get_context("fork")
+        with ctx.Pool(workers) as pool:
+            return pool.map(_make_super, blocks, chunksize=max(1, len(blocks) // (workers * 8)))
+    return [_make_super(b) for b in blocks]
+
+
+# ---------------------------------------------------------------- checks
+
+
+def _walk_bound(sd: SuperDomain) -> int:
+    """max over j of sum_l |c_l| tau^l: bounds every value the reference's
+    packet walk (straightforward_shift seeds + tabulated steps) produces."""
+    best = 0
+    for rp in sd.r_polys:
+        best = max(best, sum(abs(as_int(c)) * sd.tau**l for l, c in enumerate(rp.coeffs)))
+    return best
+
+
+def _emulate_walk(sd: SuperDomain, limbs: int) -> None:
+    """Exact replay of generate_packets (polygen.py:255-271) with MPInt
+    semantics; raises MPOverflowError where the reference would."""
+    for rp in sd.r_polys:
+        mp = BinomialPoly(tuple(MPInt.from_int(as_int(c), limbs) for c in rp.coeffs), rp.scale)
+        for u in range(sd.mu):
+            col = list(straightforward_shift(mp, u * sd.nu).coeffs)
+            for i in range(1, sd.nu):
+                for l in range(len(col) - 1):
+                    col[l] = col[l] + col[l + 1]
+
+
+def domain_poly(sd: SuperDomain, i: int) -> tuple[int, ...]:
+    """(s_0..s_delta) of domain i: r_j(i) by exact evaluation (equals the walk)."""
+    return tuple(as_int(BinomialPoly(tuple(as_int(c) for c in rp.coeffs)).evaluate(i)) for rp in sd.r_polys)
+
+
+def eps_dprime(sd: SuperDomain, count: int, frac_bits: int) -> Fraction:
+    s2 = abs(as_int(sd.r_polys[2].coeffs[0])) if len(sd.r_polys) > 2 else 0
+    return sd.eps_prime + Fraction(s2 * (count - 1) ** 2, 1 << frac_bits)
+
+
+def check_super(sd: SuperDomain, fmt: FpFormat, pg: PolyGenConfig, word_bits: int,
+                budget_ceiling: Fraction | None) -> bool:
+    """Raise exactly where the reference's phase 1 would for this block;
+    return whether phase-2 shifts are overflow-free by bound."""
+    limbs = pg.limbs
+    bound = _walk_bound(sd)
+    if bound >> (LIMB_BITS * limbs) or (sd.tau * sd.tau) >> (LIMB_BITS * limbs):
+        _emulate_walk(sd, limbs)
+    # phase-1 budget at the largest count of the block (eps'' grows with count)
+    n = max(sd.n_p if sd.tau > 1 else sd.last_count, sd.last_count)
+    e_dp = eps_dprime(sd, n, pg.frac_bits)
+    ErrorBudget(fmt.eps, sd.eps_prime - fmt.eps, e_dp - sd.eps_prime, Fraction(0))  # raises >= 1/4
+    if budget_ceiling is not None and e_dp > budget_ceiling:
+        raise ValueError("domain budget exceeds the configured ceiling")
+    pad = -((-e_dp.numerator << word_bits) // e_dp.denominator) + n + 1
+    if 2 * pad >= 1 << (word_bits - 1):
+        raise ValueError("eps must be < 1/2")
+    # phase-2 shift bound: |s_l| <= bound, shift by < n_p
+    b2 = sum(bound * sd.n_p**l for l in range(len(sd.r_polys)))
+    return not (b2 >> (LIMB_BITS * limbs))
+
+
+def check_phase2_exact(sd: SuperDomain, i: int, split: int, limbs: int) -> None:
+    """Exact MPInt replay of phase 2's straightforward_shift for one failing
+    domain (used only when the cheap bound could not rule overflow out)."""
+    s = domain_poly(sd, i)
+    poly = BinomialPoly(tuple(MPInt.from_int(v, limbs) for v in s))
+    n = sd.domain_count(i)
+    step = max(n // split, 1)
+    for start in range(0, n, step):
+        straightforward_shift(poly, start)
+
+
+# ---------------------------------------------------------------- packing
+
+
+@dataclass
+class SliceBatch:
+    """Host-side hrb_slice (include/hrb200.h) plus the metadata the host
+    needs to map results back (domain ids, argument indices)."""
+
+    supers: list
+    fmt: FpFormat
+    binade: int
+    frac_bits: int
+    word_bits: int
+    delta: int
+    limbs: int
+    coef: np.ndarray        # uint32 [6, CL, S]
+    G: np.ndarray           # uint64 [2, S]
+    s2abs: np.ndarray       # uint64 [2, S]
+    n_dom: np.ndarray       # uint32 [S]
+    dom_n: np.ndarray       # uint32 [S]
+    last_n: np.ndarray      # uint32 [S]
+    dom_base: np.ndarray    # uint64 [S+1]
+    m0: np.ndarray          # uint64 [S]
+    id0: int = 0
+    shift_bound_ok: np.ndarray = field(default=None)  # bool [S]
+
+    @property
+    def n_super(self) -> int:
+        return len(self.n_dom)
+
+    @property
+    def n_total(self) -> int:
+        return int(self.dom_base[-1])
+
+    @property
+    def coef_limbs(self) -> int:
+        return self.coef.shape[1]
+
+    @property
+    def max_dom_n(self) -> int:
+        return int(max(self.dom_n.max(), self.last_n.max()))
+
+    @property
+    def arguments(self) -> int:
+        return int(sum(s.count for s in self.supers))
+
+    def locate(self, local_ids: np.ndarray):
+        """(super index, domain index within it) of slice-local ids."""
+        t = np.searchsorted(self.dom_base, local_ids, side="right") - 1
+        return t, local_ids - self.dom_base[t]
+
+    def domain_sizes(self, local_ids: np.ndarray) -> np.ndarray:
+        t, i = self.locate(np.asarray(local_ids, dtype=np.uint64))
+        return np.where(i == self.n_dom[t].astype(np.uint64) - 1, self.last_n[t], self.dom_n[t]).astype(np.uint64)
+
+    def nbytes(self) -> int:
+        return sum(a.nbytes for a in (self.coef, self.G, self.s2abs, self.n_dom, self.dom_n, self.last_n,
+                                      self.dom_base, self.m0))
+
+
+def _limbs_of(v: int, cl: int) -> list[int]:
+    v &= (1 << (32 * cl)) - 1  # two's complement over cl limbs
+    return [(v >> (32 * l)) & 0xFFFFFFFF for l in range(cl)]
+
+
+COEF_SLOTS = ((0, 0), (0, 1), (0, 2), (1, 0), (1, 1), (2, 0))  # (j, l) of coef rows
+
+
+def pack_slice(supers: Sequence[SuperDomain], fmt: FpFormat, pg: PolyGenConfig, word_bits: int,
+               binade: int, budget_ceiling: Fraction | None = None, check: bool = True) -> SliceBatch:
+    if not supers:
+        raise ValueError("empty slice")
+    F = pg.frac_bits
+    if not word_bits <= F <= 128:
+        raise ValueError(f"the B200 path needs word_bits <= frac_bits <= 128 (got F={F}, W={word_bits})")
+    S = len(supers)
+    cl = pg.limbs + 1  # MPInt magnitude < 2^(32 L) fits L+1 two's complement limbs
+    coef = np.zeros((6, cl, S), dtype=np.uint32)
+    G = np.zeros((2, S), dtype=np.uint64)
+    s2 = np.zeros((2, S), dtype=np.uint64)
+    n_dom = np.zeros(S, dtype=np.uint32)
+    dom_n = np.zeros(S, dtype=np.uint32)
+    last_n = np.zeros(S, dtype=np.uint32)
+    m0 = np.zeros(S, dtype=np.uint64)
+    ok2 = np.ones(S, dtype=bool)
+    m128 = (1 << 64) - 1
+    for t, sd in enumerate(supers):
+        if check:
+            ok2[t] = check_super(sd, fmt, pg, word_bits, budget_ceiling)
+        for row, (j, l) in enumerate(COEF_SLOTS):
+            if j < len(sd.r_polys) and l < len(sd.r_polys[j].coeffs):
+                coef[row, :, t] = _limbs_of(as_int(sd.r_polys[j].coeffs[l]), cl)
+        g = -((-sd.eps_prime.numerator << F) // sd.eps_prime.denominator)  # ceil(eps' 2^F)
+        G[0, t], G[1, t] = g & m128, g >> 64
+        if len(sd.r_polys) > 2:
+            a = min(abs(as_int(sd.r_polys[2].coeffs[0])), (1 << 128) - 1)
+            s2[0, t], s2[1, t] = a & m128, a >> 64
+        n_dom[t], dom_n[t], last_n[t] = sd.tau, sd.n_p, sd.last_count
+        m0[t] = sd.index_start
+    dom_base = np.zeros(S + 1, dtype=np.uint64)
+    np.cumsum(n_dom, out=dom_base[1:])
+    return SliceBatch(list(supers), fmt, binade, F, word_bits, pg.delta, pg.limbs, coef, G, s2, n_dom, dom_n,
+                      last_n, dom_base, m0, id0=supers[0].dom_id0, shift_bound_ok=ok2)
+
+
+def slice_view(batch: SliceBatch, t0: int, t1: int) -> SliceBatch:
+    """Contiguous sub-slice of super-domains [t0, t1) (a shard)."""
+    db = batch.dom_base[t0:t1 + 1] - batch.dom_base[t0]
+    return SliceBatch(batch.supers[t0:t1], batch.fmt, batch.binade, batch.frac_bits, batch.word_bits,
+                      batch.delta, batch.limbs, np.ascontiguousarray(batch.coef[:, :, t0:t1]),
+                      np.ascontiguousarray(batch.G[:, t0:t1]), np.ascontiguousarray(batch.s2abs[:, t0:t1]),
+                      batch.n_dom[t0:t1].copy(), batch.dom_n[t0:t1].copy(), batch.last_n[t0:t1].copy(),
+                      db, batch.m0[t0:t1].copy(), id0=batch.id0 + int(batch.dom_base[t0]),
+                      shift_bound_ok=batch.shift_bound_ok[t0:t1].copy())
+
+
+def default_workers() -> int:
+    return max(1, min(os.cpu_count() or 1, 64))

@@ -1,0 +1,180 @@
+"""GPU parity: the CUDA path (libhrb200 via the C-ABI) against the reference's
+golden vectors and the CPU oracle.  Integer work, so every comparison is
+bit-exact."""
+
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import oracle
+from golden_io import CORE_COLUMNS, MODE_CODE, batch_of, case, config_of, essence, load_search, pipeline_cases
+
+pytestmark = pytest.mark.gpu
+
+ALGO_CODE = {"lefevre": 0, "lefevre_swap": 1, "regular": 2, "regular_unrolled": 3}
+
+
+def gpu_search(algo, mode, W, a, b, e, n):
+    from paper_1211_3056_b200.device import search_batch_arrays
+
+    return search_batch_arrays(ALGO_CODE[algo], mode, W, a, b, e, n)
+
+
+@pytest.mark.parametrize("fixture,W", [("search_w64.npz", 64), ("search_w32.npz", 32)])
+def test_search_batch_matches_reference_goldens(fixture, W):
+    g = load_search(fixture)
+    for col, (algo, mode) in enumerate(CORE_COLUMNS):
+        ok, d, it, pl, ph = gpu_search(algo, mode, W, g["a"], g["b"], g["eps"], g["count"])
+        bad = np.nonzero((ok != g["ok"][:, col]) | (d != g["d"][:, col]) | (it != g["it"][:, col])
+                         | (pl != g["pts_lo"][:, col]) | (ph.astype(np.uint64) != g["pts_hi"][:, col]))[0]
+        assert bad.size == 0, (fixture, algo, mode, bad[:5].tolist(),
+                               [(int(g["a"][k]), int(g["b"][k]), int(g["eps"][k]), int(g["count"][k])) for k in bad[:3]])
+
+
+@pytest.mark.parametrize("algo,mode", [("regular", 1), ("regular_unrolled", 1), ("lefevre", 0), ("lefevre", 1),
+                                       ("lefevre", 2), ("lefevre_swap", 1)])
+def test_search_batch_random_vs_oracle(algo, mode):
+    rng = np.random.default_rng(1234 + ALGO_CODE[algo] * 3 + mode)
+    n = 1 << 20
+    a = rng.integers(0, 2**64, n, dtype=np.uint64)
+    b = rng.integers(0, 2**64, n, dtype=np.uint64)
+    e = rng.integers(1, 2**36, n, dtype=np.uint64)
+    N = rng.choice(np.array([1, 2, 3, 17, 1 << 12, 1 << 15, 1 << 16], dtype=np.uint64), n)
+    got = gpu_search(algo, mode, 64, a, b, e, N)
+    want = oracle.search_batch(algo, mode, 1 << 64, a, b, e, N)
+    for k, name in enumerate(("ok", "d", "it", "pts_lo", "pts_hi")):
+        assert np.array_equal(got[k].astype(np.uint64), want[k].astype(np.uint64)), (algo, mode, name)
+
+
+@pytest.mark.parametrize("algo", ["lefevre", "lefevre_swap", "regular", "regular_unrolled"])
+def test_criterion2_embedded_grid_sweep(algo):
+    """test_acceptance.py:93-163 at full size on the device: every (a, b) on
+    the 2^10 grid, N in {16, 256, 1024}, embedded into W=64 words by << 54;
+    results must be the grid cores' results shifted, and Success must be
+    sound against the exact minimum."""
+    grid = 1 << 10
+    eps = grid >> 6
+    A, B = np.meshgrid(np.arange(grid, dtype=np.uint64), np.arange(grid, dtype=np.uint64), indexing="ij")
+    A, B = A.ravel(), B.ravel()
+    for n in (16, 256, 1024):
+        N = np.full(A.size, n, dtype=np.uint64)
+        E = np.full(A.size, eps, dtype=np.uint64)
+        ok, d, it, pl, ph = gpu_search(algo, 2, 64, A << np.uint64(54), B << np.uint64(54), E << np.uint64(54), N)
+        wok, wd, wit, wpl, wph = oracle.search_batch(algo, 2, grid, A, B, E, N)
+        assert np.array_equal(ok, wok)
+        assert np.array_equal(d, wd << np.uint64(54))
+        assert np.array_equal(it, wit)
+        # exact minimum over x < n for every (a, b): soundness of Success
+        x = np.arange(n, dtype=np.int64)
+        succ = np.nonzero(ok)[0]
+        av, bv = A[succ].astype(np.int64), B[succ].astype(np.int64)
+        for chunk in range(0, succ.size, 1 << 14):
+            sl = slice(chunk, chunk + (1 << 14))
+            truth = ((bv[sl, None] - av[sl, None] * x[None, :]) % grid).min(axis=1)
+            assert (truth >= eps).all()
+            assert ((d[succ][sl] >> np.uint64(54)).astype(np.int64) <= truth).all()
+
+
+@pytest.mark.parametrize("name", [c["name"] for c in pipeline_cases()])
+def test_pipeline_case_matches_reference(name):
+    from paper_1211_3056_b200.funnel import execute_batch
+
+    c = case(name)
+    cfg = config_of(c)
+    batch = batch_of(c)
+    out = execute_batch(batch, cfg, c["cfg"]["algorithm"], c["fn"])
+    assert out.failing_ids == c["phase1_fail"]
+    assert [list(r) for r in out.sub_rows] == [r[:4] for r in c["phase2"]]
+    assert [[hex(x.argument), x.distance.raw, x.domain_id] for x in out.candidates] == c["phase3"]
+    assert essence(out.records) == c["records"]
+    st = {r.phase: r for r in out.stats.rows}
+    assert [st["phase1"].domains_in, st["phase1"].domains_out, st["phase1"].arguments_covered] == c["stats"]["phase1"]
+    assert [st["phase2"].domains_in, st["phase2"].domains_out, st["phase2"].arguments_covered] == c["stats"]["phase2"]
+    assert [st["phase3"].domains_in, st["phase3"].domains_out, st["phase3"].arguments_covered] == c["stats"]["phase3"]
+
+
+@pytest.mark.parametrize("name", ["p13_exp_b0", "p53_exp_2p20_e16_N12", "p53_exp_ragged", "p53_exp_delta1"])
+def test_tabulated_values_match_reference(name):
+    """hrb_domain_coefficients (full-width add-with-carry walk) equals the
+    reference's domain_coefficient_sets value for value."""
+    from paper_1211_3056_b200.device import DeviceSlice, domain_coefficients
+
+    c = case(name)
+    batch = batch_of(c)
+    raw = domain_coefficients(DeviceSlice(batch))
+    cl = raw.shape[1]
+    for k, dom in enumerate(c["domains"]):
+        for j, hx in enumerate(dom[3:]):
+            v = 0
+            for l in range(cl):
+                v |= int(raw[j, l, k]) << (32 * l)
+            if v >> (32 * cl - 1):
+                v -= 1 << (32 * cl)
+            assert v == int(hx, 16), (name, k, j)
+
+
+@pytest.mark.parametrize("name", ["p53_exp_2p20_e16_N12", "p53_exp_ragged", "p13_log_b0"])
+def test_fused_and_host_paths_equal_phase_path(name):
+    from paper_1211_3056_b200.device import DeviceSlice, FusedRunner, run_host, run_phases
+
+    c = case(name)
+    batch = batch_of(c)
+    algo = ALGO_CODE[c["cfg"]["algorithm"]]
+    mode = MODE_CODE[c["cfg"]["div_mode"]]
+    split = c["cfg"]["split"]
+    ds = DeviceSlice(batch)
+    ref = run_phases(ds, algo, mode, split)
+    fused = FusedRunner(ds, algo, mode, split, sub_cap=batch.n_total * 2 * split, cand_cap=1 << 16)
+    for _ in range(2):  # re-launch on the same buffers: no stale state
+        fused.launch()
+        r = fused.result()
+        assert np.array_equal(r.fail_ids, ref.fail_ids)
+        assert np.array_equal(r.sub_keys, ref.sub_keys)
+        assert np.array_equal(r.cand_index, ref.cand_index)
+        assert np.array_equal(r.cand_dist, ref.cand_dist)
+        assert r.iterations == ref.iterations
+    counts, fail, cm, cd, cdom, ms = run_host(batch, algo, mode, split)
+    assert np.array_equal(fail, ref.fail_ids)
+    assert np.array_equal(cm, ref.cand_index) and np.array_equal(cd, ref.cand_dist)
+    assert np.array_equal(cdom, ref.cand_dom)
+    assert ms > 0
+
+
+def test_run_pipeline_whole_binade_host_polygen():
+    """Host Taylor generation (this package) + device phases reproduce the
+    reference's run_pipeline records and stats for exp p=13 binade 0."""
+    from paper_1211_3056_b200 import run_pipeline
+
+    c = case("p13_exp_b0")
+    records, stats = run_pipeline(0, config_of(c))
+    assert essence(records) == c["records"]
+    assert len(records) == 42
+    assert [r.phase for r in stats.rows] == ["phase1", "phase2", "phase3", "confirm"]
+
+
+def test_per_phase_dropins():
+    """phase1 / phase2 / phase3_exhaustive over explicit DomainTasks."""
+    from paper_1211_3056_b200 import Domain, DomainTask, phase1, phase2, phase3_exhaustive
+    from paper_1211_3056_b200.arith import MPInt
+
+    c = case("p13_exp_b0")
+    cfg = config_of(c)
+    m_base = 1 << (c["p"] - 1)
+    eps_of = {}
+    for s in c["supers"]:
+        for k in range(s["tau"]):
+            eps_of[s["dom_id0"] + k] = (Fraction(int(s["eps_prime"][0]), int(s["eps_prime"][1])), s["e_out"])
+    tasks = []
+    for dom in c["domains"]:
+        did, m_off, cnt = dom[0], dom[1], dom[2]
+        ep, e_out = eps_of[did]
+        tasks.append(DomainTask(Domain(m_base + m_off, c["binade"] + 1, cnt, did),
+                                tuple(MPInt.from_int(int(h, 16), 8) for h in dom[3:]), 96, ep, e_out))
+    fails = phase1(tasks, cfg, "regular")
+    assert fails == c["phase1_fail"]
+    by_id = {t.domain.domain_id: t for t in tasks}
+    subs = phase2([by_id[i] for i in fails], cfg, "regular")
+    assert [[s.parent.domain.domain_id, s.sub_index, s.start, s.count] for s in subs] == [r[:4] for r in c["phase2"]]
+    cands = phase3_exhaustive(subs, cfg)
+    assert [[hex(x.argument), x.distance.raw, x.domain_id] for x in cands] == c["phase3"]
