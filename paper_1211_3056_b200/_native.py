@@ -105,7 +105,7 @@ def load(path: str | None = None):
     with _lock:
         if _lib is not None:
             return _lib
-        path = path or LIB
+        path = path or os.environ.get("HRB_LIB") or LIB
         if not os.path.exists(path):
             from .build import build
 

@@ -30,6 +30,7 @@
 
 #include "../../include/hrb200.h"
 #include "search_core.cuh"
+#include "tile_search.cuh"
 
 using u128 = unsigned __int128;
 
@@ -54,6 +55,12 @@ int cuda_err(cudaError_t e, const char* where) {
         if (_rc) return _rc;                           \
     } while (0)
 
+#ifndef HRB_P1_MINB
+#define HRB_P1_MINB 5  // CTAs of 128 per SM for the phase-1 regular kernel
+#endif
+#ifndef HRB_P2_MINB
+#define HRB_P2_MINB 5
+#endif
 constexpr int NU = 16;             // domains per lane in phase 1 (stride-32 walk)
 constexpr int TILE = 32 * NU;      // domains per warp tile
 constexpr int CHUNK3 = 256;        // arguments per thread in phase 3
@@ -147,6 +154,16 @@ __device__ __forceinline__ int64_t find_seg(const uint64_t* base, int64_t S, uin
     return lo;
 }
 
+// t of a slice-local domain id: interpolation guess (exact when the
+// super-domains are uniform) then a short gallop/binary search
+__device__ __forceinline__ int64_t locate_super(const uint64_t* base, int64_t S, uint64_t id) {
+    const uint64_t total = __ldg(&base[S]);
+    int64_t g = total ? (int64_t)((double)id * (double)S / (double)total) : 0;
+    if (g >= S) g = S - 1;
+    if (__ldg(&base[g]) <= id && id < __ldg(&base[g + 1])) return g;
+    return find_seg(base, S, id);
+}
+
 __device__ __forceinline__ uint64_t domain_size(const SliceDev& s, int64_t t, uint64_t i) {
     uint32_t nd = __ldg(&s.n_dom[t]);
     return i == (uint64_t)nd - 1 ? __ldg(&s.last_n[t]) : __ldg(&s.dom_n[t]);
@@ -197,7 +214,8 @@ __global__ void prep_kernel(SliceDev s, int split, uint64_t* tiles, unsigned lon
 // ---------------------------------------------------------------------------
 template <int W, bool REG>
 __global__ void __launch_bounds__(256) phase1_kernel(SliceDev s, int algo, int mode, const uint64_t* tile_base,
-                                                     uint32_t* bitmap, unsigned long long* iter_sum) {
+                                                     uint32_t* bitmap, uint32_t* tile_t,
+                                                     unsigned long long* iter_sum) {
     const int lane = threadIdx.x & 31;
     const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -245,6 +263,7 @@ __global__ void __launch_bounds__(256) phase1_kernel(SliceDev s, int algo, int m
             if (lane == k) mine = w;
         }
         if (lane < NU) bitmap[gw * NU + lane] = mine;
+        if (lane == 0) tile_t[gw] = (uint32_t)t;
     }
     // warp-reduce the iteration count, one atomic per warp
     for (int o = 16; o > 0; o >>= 1) iters += __shfl_xor_sync(0xffffffffu, iters, o);
@@ -252,53 +271,237 @@ __global__ void __launch_bounds__(256) phase1_kernel(SliceDev s, int algo, int m
 }
 
 // ---------------------------------------------------------------------------
-// phase 2: per (failing domain, subdomain j): shift, re-test, bitmap
+// regular family, throughput form (tile_search.cuh): phase 1 and phase 2
 // ---------------------------------------------------------------------------
-template <int W, bool REG>
-__global__ void __launch_bounds__(256) phase2_kernel(SliceDev s, int algo, int mode, int split,
-                                                     const uint64_t* fail_ids, const uint64_t* fail_count,
-                                                     uint64_t fail_cap, const unsigned long long* meta,
-                                                     uint32_t* bitmap) {
+struct Walk {  // per-lane stride-32 difference tables, in shared memory
+    u128 g0, g1, h0;
+};
+
+// top W bits of (x mod 2^F), i.e. (x mod 2^F) >> (F - W), via one funnel
+// shift: sh = 128 - F
+template <int W>
+__device__ __forceinline__ uint64_t top_bits(u128 x, int sh) {
+    const u128 y = x << sh;
+    return W == 64 ? (uint64_t)(y >> 64) : (uint64_t)(y >> 96);
+}
+
+template <int W>
+struct WalkSrc {
+    Walk* w;
+    const u128* inc;  // per-warp constants in shared memory: {g2, h1}
+    uint64_t pad_full, pad_last;
+    uint32_t il, nd, nfull, nlast;
+    int sh;
+    __device__ __forceinline__ bool build(int k, uint64_t& a, uint64_t& b, uint64_t& eps, uint32_t& N) {
+        const uint32_t i = il + 32u * (uint32_t)k;
+        if (i >= nd) return false;
+        const bool last = i == nd - 1;
+        const u128 s0 = w->g0, s1 = w->h0, g1 = w->g1;
+        const uint64_t pad = last ? pad_last : pad_full;
+        const uint64_t wmask = W == 64 ? ~0ull : 0xFFFFFFFFull;
+        a = top_bits<W>(0 - s1, sh);
+        b = (top_bits<W>(s0, sh) + pad) & wmask;
+        eps = 2 * pad;
+        N = last ? nlast : nfull;
+        // tabulated step: three multi-word additions per domain
+        w->g0 = s0 + g1;
+        w->g1 = g1 + inc[0];
+        w->h0 = s1 + inc[1];
+        return true;
+    }
+};
+
+template <int W>
+__global__ void __launch_bounds__(128, HRB_P1_MINB) phase1_reg_kernel(SliceDev s, int algo, const uint64_t* tile_base,
+                                                          uint32_t* bitmap, uint32_t* tile_t,
+                                                          unsigned long long* iter_sum) {
+    __shared__ Walk walks[128];
+    __shared__ u128 incs[4][2];
     const int lane = threadIdx.x & 31;
-    const uint64_t J = meta[0];
+    const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const uint64_t total_tiles = tile_base[s.S];
+    unsigned long long iters = 0;
+    WalkSrc<W> src;
+    src.w = &walks[threadIdx.x];
+    src.inc = incs[threadIdx.x >> 5];
+    src.sh = 128 - s.F;
+    for (uint64_t gw = warp0; gw < total_tiles; gw += nwarps) {
+        const int64_t t = find_seg(tile_base, s.S, gw);
+        const uint64_t tile = gw - tile_base[t];
+        const u128 c00 = coef_res(s, t, 0), c01 = coef_res(s, t, 1), c02 = coef_res(s, t, 2);
+        const u128 c10 = coef_res(s, t, 3), c11 = coef_res(s, t, 4);
+        const u128 G = ld128(s.G, s.S, t);
+        const u128 s2a = s.delta >= 2 ? ld128(s.s2abs, s.S, t) : (u128)0;
+        src.nd = __ldg(&s.n_dom[t]);
+        src.nfull = __ldg(&s.dom_n[t]);
+        src.nlast = __ldg(&s.last_n[t]);
+        src.pad_full = pad_of(G, s2a, src.nfull, s.F, W);
+        src.pad_last = pad_of(G, s2a, src.nlast, s.F, W);
+        const uint64_t il = tile * TILE + lane;
+        src.il = (uint32_t)il;
+        __syncwarp();
+        src.w->g0 = c00 + c01 * (u128)il + c02 * (u128)binom2(il);
+        src.w->g1 = (c01 << 5) + c02 * (u128)(32 * il + 496);
+        src.w->h0 = c10 + c11 * (u128)il;
+        if (lane == 0) {
+            incs[threadIdx.x >> 5][0] = c02 << 10;
+            incs[threadIdx.x >> 5][1] = c11 << 5;
+        }
+        __syncwarp();
+        unsigned long long its = 0;
+        const uint32_t fails = hrb::lane_items<W, NU>(src, &its, algo == hrb::ALGO_REGULAR_UNROLLED);
+        iters += its;
+        uint32_t mine = 0;
+#pragma unroll
+        for (int k = 0; k < NU; k++) {
+            uint32_t wd = __ballot_sync(0xffffffffu, (fails >> k) & 1u);
+            if (lane == k) mine = wd;
+        }
+        if (lane < NU) bitmap[gw * NU + lane] = mine;
+        if (lane == 0) tile_t[gw] = (uint32_t)t;
+    }
+    for (int o = 16; o > 0; o >>= 1) iters += __shfl_xor_sync(0xffffffffu, iters, o);
+    if (iter_sum && lane == 0 && iters) atomicAdd(iter_sum, iters);
+}
+
+// Phase 2, one failing domain per lane: its subdomains j = 0..J-1 are the
+// lane's items.  The shifted polynomials (straightforward_shift by j*step,
+// polygen.py:143-158) are walked with tabulated differences of stride
+// `step`: t0 += dt0, dt0 += s2 step^2, t1 += s2 step (exact mod 2^128).
+template <int W>
+struct SubWalkSrc {
+    u128 t0, dt0, d2, t1, dt1;
+    uint64_t pad_full, pad_last;
+    uint32_t nsub, step, last_cnt;
+    int sh, base;  // base: first sub index of the current 32-item chunk
+    __device__ __forceinline__ bool build(int k, uint64_t& a, uint64_t& b, uint64_t& eps, uint32_t& N) {
+        const uint32_t j = (uint32_t)(base + k);
+        if (j >= nsub) return false;
+        const bool last = j == nsub - 1;
+        const uint64_t pad = last ? pad_last : pad_full;
+        const uint64_t wmask = W == 64 ? ~0ull : 0xFFFFFFFFull;
+        a = top_bits<W>(0 - t1, sh);
+        b = (top_bits<W>(t0, sh) + pad) & wmask;
+        eps = 2 * pad;
+        N = last ? last_cnt : step;
+        t0 += dt0;
+        dt0 += d2;
+        t1 += dt1;
+        return true;
+    }
+};
+
+template <int W>
+__global__ void __launch_bounds__(128, HRB_P2_MINB) phase2_reg_kernel(SliceDev s, int split, const uint64_t* fail_ids,
+                                                          const uint32_t* fail_t, const uint64_t* fail_count,
+                                                          uint64_t fail_cap, const unsigned long long* meta,
+                                                          uint32_t* bitmap) {
     uint64_t nf = *fail_count;
     if (nf > fail_cap) nf = fail_cap;
-    const uint64_t n_items = nf * J;
+    const uint32_t J = (uint32_t)meta[0];
+    const uint32_t wpd = (J + 31) >> 5;  // bitmap words per failing domain
+    SubWalkSrc<W> src;
+    src.sh = 128 - s.F;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    const u128 mF = mask_f(s.F);
-    for (uint64_t base = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) & ~31ull; base < n_items; base += stride) {
-        const uint64_t g = base + lane;
-        bool fail = false;
-        if (g < n_items) {
-            const uint64_t f = g / J, j = g - f * J;
+    // whole warps iterate together so the lockstep pairs stay converged
+    const uint64_t nf_pad = (nf + 31) & ~31ull;
+    for (uint64_t f = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; f < nf_pad; f += stride) {
+        const bool valid = f < nf;
+        src.nsub = 0;
+        if (valid) {
             const uint64_t id = fail_ids[f];
-            const int64_t t = find_seg(s.dom_base, s.S, id);
-            const uint64_t i = id - s.dom_base[t];
+            const int64_t t = fail_t[f];
+            const uint64_t i = id - __ldg(&s.dom_base[t]);
             const uint64_t n = domain_size(s, t, i);
-            uint64_t step = n / split;
+            uint64_t step = n / (uint64_t)split;
             if (step < 1) step = 1;
             const uint64_t nsub = (n + step - 1) / step;
-            if (j < nsub) {
-                const uint64_t start = j * step;
-                const uint64_t cnt = n - start < step ? n - start : step;
-                const u128 c00 = coef_res(s, t, 0), c01 = coef_res(s, t, 1), c02 = coef_res(s, t, 2);
-                const u128 c10 = coef_res(s, t, 3), c11 = coef_res(s, t, 4), c20 = coef_res(s, t, 5);
-                // domain polynomial (s0, s1, s2) at i, then straightforward_shift by start
-                const u128 s0 = c00 + c01 * (u128)i + c02 * (u128)binom2(i);
-                const u128 s1 = c10 + c11 * (u128)i;
-                const u128 s2 = s.delta >= 2 ? c20 : (u128)0;
-                const u128 t0 = s0 + s1 * (u128)start + s2 * (u128)binom2(start);
-                const u128 t1 = s1 + s2 * (u128)start;
-                const u128 G = ld128(s.G, s.S, t);
-                const u128 s2a = s.delta >= 2 ? ld128(s.s2abs, s.S, t) : (u128)0;
-                Problem p = make_problem(t0, t1, pad_of(G, s2a, cnt, s.F, W), s.F, W, mF);
-                hrb::Outcome o = search_one<W, REG>(algo, mode, p, cnt);
-                fail = !o.ok;
-            }
+            const u128 c00 = coef_res(s, t, 0), c01 = coef_res(s, t, 1), c02 = coef_res(s, t, 2);
+            const u128 c10 = coef_res(s, t, 3), c11 = coef_res(s, t, 4);
+            const u128 s2 = s.delta >= 2 ? coef_res(s, t, 5) : (u128)0;
+            const u128 s0 = c00 + c01 * (u128)i + c02 * (u128)binom2(i);  // P_{t+i} = r_j(i)
+            const u128 s1 = c10 + c11 * (u128)i;
+            const u128 G = ld128(s.G, s.S, t);
+            const u128 s2a = s.delta >= 2 ? ld128(s.s2abs, s.S, t) : (u128)0;
+            src.t0 = s0;
+            src.dt0 = s1 * (u128)step + s2 * (u128)binom2(step);
+            src.d2 = s2 * (u128)(step * step);
+            src.t1 = s1;
+            src.dt1 = s2 * (u128)step;
+            src.nsub = (uint32_t)nsub;
+            src.step = (uint32_t)step;
+            src.last_cnt = (uint32_t)(n - (nsub - 1) * step);
+            src.pad_full = pad_of(G, s2a, step, s.F, W);
+            src.pad_last = pad_of(G, s2a, src.last_cnt, s.F, W);
         }
-        uint32_t w = __ballot_sync(0xffffffffu, fail);
-        if (lane == 0 && base < n_items) bitmap[base >> 5] = w;
+        for (uint32_t c = 0; c < wpd; c++) {
+            src.base = 32 * c;
+            unsigned long long its = 0;
+            const uint32_t fails = hrb::lane_items<W, 32>(src, &its, false, src.nsub > 32 * c ? src.nsub - 32 * c : 0);
+            if (valid) bitmap[f * wpd + c] = fails;
+        }
     }
+}
+
+// Phase 2 for the classic family: one failing domain per thread, its
+// subdomains searched one after another (the classic walk's heavy-tailed
+// iteration counts gain nothing from lockstep pairing).
+template <int W>
+__global__ void __launch_bounds__(256) phase2_classic_kernel(SliceDev s, int mode, int split, const uint64_t* fail_ids,
+                                                             const uint32_t* fail_t, const uint64_t* fail_count,
+                                                             uint64_t fail_cap, const unsigned long long* meta,
+                                                             uint32_t* bitmap) {
+    uint64_t nf = *fail_count;
+    if (nf > fail_cap) nf = fail_cap;
+    const uint32_t wpd = ((uint32_t)meta[0] + 31) >> 5;
+    for (uint64_t f = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; f < nf; f += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t id = fail_ids[f];
+        const int64_t t = fail_t[f];
+        const uint64_t i = id - __ldg(&s.dom_base[t]);
+        const uint64_t n = domain_size(s, t, i);
+        uint64_t step = n / (uint64_t)split;
+        if (step < 1) step = 1;
+        const uint64_t nsub = (n + step - 1) / step;
+        const u128 c00 = coef_res(s, t, 0), c01 = coef_res(s, t, 1), c02 = coef_res(s, t, 2);
+        const u128 c10 = coef_res(s, t, 3), c11 = coef_res(s, t, 4);
+        const u128 s2 = s.delta >= 2 ? coef_res(s, t, 5) : (u128)0;
+        const u128 G = ld128(s.G, s.S, t);
+        const u128 s2a = s.delta >= 2 ? ld128(s.s2abs, s.S, t) : (u128)0;
+        SubWalkSrc<W> src;
+        src.sh = 128 - s.F;
+        src.t0 = c00 + c01 * (u128)i + c02 * (u128)binom2(i);
+        src.t1 = c10 + c11 * (u128)i;
+        src.dt0 = src.t1 * (u128)step + s2 * (u128)binom2(step);
+        src.d2 = s2 * (u128)(step * step);
+        src.dt1 = s2 * (u128)step;
+        src.nsub = (uint32_t)nsub;
+        src.step = (uint32_t)step;
+        src.last_cnt = (uint32_t)(n - (nsub - 1) * step);
+        src.pad_full = pad_of(G, s2a, step, s.F, W);
+        src.pad_last = pad_of(G, s2a, src.last_cnt, s.F, W);
+        for (uint32_t c = 0; c < wpd; c++) {
+            src.base = 32 * c;
+            uint32_t fails = 0;
+            for (int k = 0; k < 32; k++) {
+                uint64_t a, b, eps;
+                uint32_t N;
+                if (!src.build(k, a, b, eps, N)) break;
+                if (!hrb::lefevre_search<W>(a, b, eps, N, mode).ok) fails |= 1u << k;
+            }
+            bitmap[f * wpd + c] = fails;
+        }
+    }
+}
+
+// t of each listed slice-local id (standalone ABI calls; the fused path gets
+// t from the compaction instead)
+__global__ void locate_kernel(const uint64_t* base, int64_t S, const uint64_t* ids, const uint64_t* count,
+                              uint64_t cap, int shift, uint32_t* out_t) {
+    uint64_t n = *count;
+    if (n > cap) n = cap;
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n; k += (uint64_t)gridDim.x * blockDim.x)
+        out_t[k] = (uint32_t)locate_super(base, S, ids[k] >> shift);
 }
 
 // ---------------------------------------------------------------------------
@@ -309,10 +512,19 @@ struct Cand {
     uint32_t rank;
 };
 
+// Phase 3 walk, scaled form: with sh = 128 - F the registers hold
+// V = (v + window - 1) 2^sh, D1 = d1 2^sh, D2 = d2 2^sh, so the mod-2^F
+// walk of pipeline.py:291-292 is plain 128-bit wraparound and the
+// two-sided window test of pipeline.py:281 (v < window or v > 2^F - window)
+// is the single unsigned compare V < (2 window - 1) 2^sh.  Hits are rare
+// (~2 eps' per argument): a lane ORs its hits over 32 arguments, and only
+// when some lane of the warp hit does the warp re-walk those 32 arguments
+// and append the candidates with __ballot_sync/__popc (one atomic per warp).
 __global__ void __launch_bounds__(256) phase3_kernel(SliceDev s, int split, const uint64_t* sub_keys,
-                                                     const uint64_t* sub_count, uint64_t sub_cap,
-                                                     const unsigned long long* meta, uint32_t* item_counts,
-                                                     Cand* app, unsigned long long* app_count, uint64_t app_cap) {
+                                                     const uint32_t* sub_t, const uint64_t* sub_count,
+                                                     uint64_t sub_cap, const unsigned long long* meta,
+                                                     uint32_t* item_counts, Cand* app, unsigned long long* app_count,
+                                                     uint64_t app_cap) {
     const int lane = threadIdx.x & 31;
     const uint64_t maxstep = meta[1];
     const uint64_t CH = (maxstep + CHUNK3 - 1) / CHUNK3;
@@ -321,18 +533,18 @@ __global__ void __launch_bounds__(256) phase3_kernel(SliceDev s, int split, cons
     const uint64_t n_items = ns * CH;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     const int F = s.F;
-    const u128 mF = mask_f(F);
-    const u128 oneF = F >= 128 ? (u128)0 : ((u128)1 << F);
+    const int sh = 128 - F;
     for (uint64_t base = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) & ~31ull; base < n_items; base += stride) {
         const uint64_t g = base + lane;
-        uint64_t len = 0, mbase = 0, dom = 0;
-        u128 v = 0, d1 = 0, d2 = 0, window = 1;
+        uint32_t len = 0;
+        uint64_t mbase = 0, dom = 0;
+        u128 V = 0, D1 = 0, D2 = 0, K = 0, wm1 = 0;
         if (g < n_items) {
             const uint64_t r = g / CH, c = g - r * CH;
             const uint64_t key = sub_keys[r];
             dom = key >> 8;
             const uint64_t j = key & 255;
-            const int64_t t = find_seg(s.dom_base, s.S, dom);
+            const int64_t t = sub_t[r];
             const uint64_t i = dom - s.dom_base[t];
             const uint64_t n = domain_size(s, t, i);
             uint64_t step = n / split;
@@ -341,49 +553,62 @@ __global__ void __launch_bounds__(256) phase3_kernel(SliceDev s, int split, cons
             const uint64_t cnt = n - start < step ? n - start : step;
             const uint64_t x0 = c * CHUNK3;
             if (x0 < cnt) {
-                len = cnt - x0 < CHUNK3 ? cnt - x0 : CHUNK3;
+                len = (uint32_t)(cnt - x0 < CHUNK3 ? cnt - x0 : CHUNK3);
                 const uint64_t o = start + x0;
                 const u128 c00 = coef_res(s, t, 0), c01 = coef_res(s, t, 1), c02 = coef_res(s, t, 2);
-                const u128 c10 = coef_res(s, t, 3), c11 = coef_res(s, t, 4), c20 = coef_res(s, t, 5);
+                const u128 c10 = coef_res(s, t, 3), c11 = coef_res(s, t, 4);
+                const u128 s2 = s.delta >= 2 ? coef_res(s, t, 5) : (u128)0;
                 const u128 s0 = c00 + c01 * (u128)i + c02 * (u128)binom2(i);
                 const u128 s1 = c10 + c11 * (u128)i;
-                const u128 s2 = s.delta >= 2 ? c20 : (u128)0;
-                v = s0 + s1 * (u128)o + s2 * (u128)binom2(o);  // P(o)
-                d1 = s1 + s2 * (u128)o;                        // Delta P(o)
-                d2 = s2;
-                window = ld128(s.G, s.S, t) + 1;  // ceil(eps' 2^F) + 1  (pipeline.py:274)
+                const u128 window = ld128(s.G, s.S, t) + 1;  // ceil(eps' 2^F) + 1 (pipeline.py:274)
+                wm1 = window - 1;
+                V = (s0 + s1 * (u128)o + s2 * (u128)binom2(o) + wm1) << sh;  // P(o), shifted origin
+                D1 = (s1 + s2 * (u128)o) << sh;                             // Delta P(o)
+                D2 = s2 << sh;
+                K = (2 * window - 1) << sh;
                 mbase = __ldg(&s.m0[t]) + i * (uint64_t)__ldg(&s.dom_n[t]) + o;
             }
         }
-        const u128 hiw = (oneF - window) & mF;
         uint32_t rank = 0;
-        for (int x = 0; x < CHUNK3; x++) {
-            const u128 vm = v & mF;
-            const bool hit = (uint64_t)x < len && (vm < window || vm > hiw);
-            if (__any_sync(0xffffffffu, hit)) {
-                const uint32_t ball = __ballot_sync(0xffffffffu, hit);
-                const int leader = __ffs(ball) - 1;
-                unsigned long long pos = 0;
-                if (lane == leader) pos = atomicAdd(app_count, (unsigned long long)__popc(ball));
-                pos = __shfl_sync(0xffffffffu, pos, leader);
-                if (hit) {
-                    pos += __popc(ball & ((1u << lane) - 1));
-                    if (pos < app_cap) {
-                        const u128 comp = (oneF - vm) & mF;
-                        const u128 dist = (vm == 0 || vm < comp) ? vm : comp;
-                        Cand cd;
-                        cd.m = mbase + x;
-                        cd.dist = F >= 64 ? (uint64_t)(dist >> (F - 64)) : (uint64_t)(dist << (64 - F));
-                        cd.dom = dom;
-                        cd.item = g;
-                        cd.rank = rank;
-                        app[pos] = cd;
+        for (uint32_t x0 = 0; x0 < CHUNK3; x0 += 32) {
+            const u128 V0 = V, D10 = D1;
+            bool any = false;
+#pragma unroll 8
+            for (uint32_t x = 0; x < 32; x++) {
+                any |= (x0 + x < len) && V < K;
+                V += D1;
+                D1 += D2;
+            }
+            if (__any_sync(0xffffffffu, any)) {  // rare: re-walk and append in order
+                u128 v = V0, d = D10;
+                for (uint32_t x = 0; x < 32; x++) {
+                    const bool hit = (x0 + x < len) && v < K;
+                    const uint32_t ball = __ballot_sync(0xffffffffu, hit);
+                    if (ball) {
+                        const int leader = __ffs(ball) - 1;
+                        unsigned long long pos = 0;
+                        if (lane == leader) pos = atomicAdd(app_count, (unsigned long long)__popc(ball));
+                        pos = __shfl_sync(0xffffffffu, pos, leader) + __popc(ball & ((1u << lane) - 1));
+                        if (hit) {
+                            if (pos < app_cap) {
+                                const u128 vv = ((v >> sh) - wm1) & mask_f(F);
+                                const u128 comp = (F >= 128 ? (u128)0 - vv : (((u128)1 << F) - vv)) & mask_f(F);
+                                const u128 dist = (vv == 0 || vv < comp) ? vv : comp;
+                                Cand cd;
+                                cd.m = mbase + x0 + x;
+                                cd.dist = F >= 64 ? (uint64_t)(dist >> (F - 64)) : (uint64_t)(dist << (64 - F));
+                                cd.dom = dom;
+                                cd.item = g;
+                                cd.rank = rank;
+                                app[pos] = cd;
+                            }
+                            rank++;
+                        }
                     }
-                    rank++;
+                    v += d;
+                    d += D2;
                 }
             }
-            v += d1;
-            d1 += d2;
         }
         if (g < n_items) item_counts[g] = rank;
     }
@@ -392,55 +617,63 @@ __global__ void __launch_bounds__(256) phase3_kernel(SliceDev s, int split, cons
 // ---------------------------------------------------------------------------
 // ordered compaction: 3-kernel reduce / scan / scatter with a device-side size
 // ---------------------------------------------------------------------------
-struct P1Compact {  // bitmap of padded domain indices -> slice-local ids
+struct P1Compact {  // bitmap of padded domain indices -> slice-local ids (+ t)
     const uint32_t* bm;
     const uint64_t* tile_base;
+    const uint32_t* tile_t;
     const uint64_t* dom_base;
     int64_t S;
     uint64_t* out;
+    uint32_t* out_t;
     uint64_t cap;
     __device__ uint64_t size() const { return tile_base[S] * NU; }
     __device__ uint32_t count(uint64_t w) const { return __popc(bm[w]); }
     __device__ void emit(uint64_t w, uint64_t off) const {
         uint32_t x = bm[w];
+        const uint64_t gw = w / NU;
+        const uint32_t t = tile_t[gw];
+        const uint64_t first = dom_base[t] + (gw - tile_base[t]) * TILE + (w - gw * NU) * 32;
         while (x) {
             int b = __ffs(x) - 1;
             x &= x - 1;
             if (off < cap) {
-                uint64_t P = w * 32 + b;
-                uint64_t gw = P / TILE;
-                int64_t t = find_seg(tile_base, S, gw);
-                out[off] = dom_base[t] + (P - tile_base[t] * TILE);
+                out[off] = first + b;
+                out_t[off] = t;
             }
             off++;
         }
     }
 };
 
-struct P2Compact {  // bitmap over (f, j) items -> (id << 8 | j)
+struct P2Compact {  // bitmap over (f, j) items -> (id << 8 | j) (+ t)
     const uint32_t* bm;
     const uint64_t* fail_ids;
+    const uint32_t* fail_t;
     const uint64_t* fail_count;
     uint64_t fail_cap;
     const unsigned long long* meta;
     uint64_t* out;
+    uint32_t* out_t;
     uint64_t cap;
     __device__ uint64_t size() const {
         uint64_t nf = *fail_count;
         if (nf > fail_cap) nf = fail_cap;
-        return (nf * meta[0] + 31) >> 5;
+        return nf * ((meta[0] + 31) >> 5);
     }
     __device__ uint32_t count(uint64_t w) const { return __popc(bm[w]); }
     __device__ void emit(uint64_t w, uint64_t off) const {
         uint32_t x = bm[w];
-        const uint64_t J = meta[0];
+        const uint64_t wpd = (meta[0] + 31) >> 5;
+        const uint64_t f = w / wpd;
+        const uint64_t j0 = (w - f * wpd) * 32;
+        const uint64_t id = fail_ids[f];
+        const uint32_t t = fail_t[f];
         while (x) {
             int b = __ffs(x) - 1;
             x &= x - 1;
             if (off < cap) {
-                uint64_t g = w * 32 + b;
-                uint64_t f = g / J;
-                out[off] = (fail_ids[f] << 8) | (g - f * J);
+                out[off] = (id << 8) | (j0 + b);
+                out_t[off] = t;
             }
             off++;
         }
@@ -651,7 +884,7 @@ struct Buf {
 };
 
 struct Workspace {
-    Buf tiles, tile_base, meta, bm1, bm2, blocks, total, counts3, offs3, app, appc, cub_tmp, fail_cnt_tmp;
+    Buf tiles, tile_base, meta, bm1, bm2, blocks, counts3, offs3, app, appc, cub_tmp, tile_t, fail_t, sub_t;
 };
 
 std::mutex g_ws_mu;
@@ -722,47 +955,62 @@ int phase1_impl(Workspace& ws, const hrb_slice* s, const SliceDev& sd, int algo,
     // upper bound of tiles: n_total/TILE + S
     const uint64_t max_tiles = (uint64_t)s->n_total / TILE + (uint64_t)s->n_super + 1;
     if ((rc = ws.bm1.ensure(sizeof(uint32_t) * max_tiles * NU))) return rc;
+    if ((rc = ws.tile_t.ensure(sizeof(uint32_t) * max_tiles))) return rc;
+    if ((rc = ws.fail_t.ensure(sizeof(uint32_t) * (cap + 1)))) return rc;
     const int grid = sm_count() * 8;
-    const bool reg = algo >= hrb::ALGO_REGULAR;
     auto tb = (const uint64_t*)ws.tile_base.p;
     auto bm = (uint32_t*)ws.bm1.p;
+    auto tt = (uint32_t*)ws.tile_t.p;
     auto is = (unsigned long long*)iter_sum;
-    if (sd.W == 64 && reg) phase1_kernel<64, true><<<grid, 256, 0, st>>>(sd, algo, mode, tb, bm, is);
-    else if (sd.W == 64) phase1_kernel<64, false><<<grid, 256, 0, st>>>(sd, algo, mode, tb, bm, is);
-    else if (reg) phase1_kernel<32, true><<<grid, 256, 0, st>>>(sd, algo, mode, tb, bm, is);
-    else phase1_kernel<32, false><<<grid, 256, 0, st>>>(sd, algo, mode, tb, bm, is);
+    if (algo >= hrb::ALGO_REGULAR) {
+        const int g5 = sm_count() * HRB_P1_MINB;  // persistent: one wave at the launch bound
+        if (sd.W == 64) phase1_reg_kernel<64><<<g5, 128, 0, st>>>(sd, algo, tb, bm, tt, is);
+        else phase1_reg_kernel<32><<<g5, 128, 0, st>>>(sd, algo, tb, bm, tt, is);
+    } else {
+        if (sd.W == 64) phase1_kernel<64, false><<<grid, 256, 0, st>>>(sd, algo, mode, tb, bm, tt, is);
+        else phase1_kernel<32, false><<<grid, 256, 0, st>>>(sd, algo, mode, tb, bm, tt, is);
+    }
     CK(cudaGetLastError());
-    P1Compact fn{(const uint32_t*)ws.bm1.p, (const uint64_t*)ws.tile_base.p, s->dom_base, sd.S, fail_ids, cap};
+    P1Compact fn{(const uint32_t*)ws.bm1.p, tb, tt, s->dom_base, sd.S, fail_ids, (uint32_t*)ws.fail_t.p, cap};
     return run_compact(ws, fn, fail_count, st);
 }
 
+// fail_t == nullptr: locate the super-domains of caller-provided ids first
 int phase2_impl(Workspace& ws, const hrb_slice* s, const SliceDev& sd, int algo, int mode, int split,
-                const uint64_t* fail_ids, const uint64_t* fail_count, uint64_t fail_cap, uint64_t* sub_keys,
-                uint64_t* sub_count, uint64_t cap, cudaStream_t st) {
+                const uint64_t* fail_ids, const uint32_t* fail_t, const uint64_t* fail_count, uint64_t fail_cap,
+                uint64_t* sub_keys, uint64_t* sub_count, uint64_t cap, cudaStream_t st) {
     int rc;
     const uint64_t Jmax = 2 * (uint64_t)split;
-    if ((rc = ws.bm2.ensure(sizeof(uint32_t) * ((fail_cap * Jmax + 31) / 32 + 1)))) return rc;
+    if ((rc = ws.bm2.ensure(sizeof(uint32_t) * (fail_cap + 1) * ((Jmax + 31) / 32)))) return rc;
+    if ((rc = ws.sub_t.ensure(sizeof(uint32_t) * (cap + 1)))) return rc;
+    if (!fail_t) {
+        if ((rc = ws.fail_t.ensure(sizeof(uint32_t) * (fail_cap + 1)))) return rc;
+        locate_kernel<<<sm_count() * 4, 256, 0, st>>>(s->dom_base, sd.S, fail_ids, fail_count, fail_cap, 0,
+                                                      (uint32_t*)ws.fail_t.p);
+        fail_t = (const uint32_t*)ws.fail_t.p;
+    }
     const int grid = sm_count() * 8;
-    const bool reg = algo >= hrb::ALGO_REGULAR;
     auto mt = (const unsigned long long*)ws.meta.p;
     auto bm = (uint32_t*)ws.bm2.p;
-    if (sd.W == 64 && reg)
-        phase2_kernel<64, true><<<grid, 256, 0, st>>>(sd, algo, mode, split, fail_ids, fail_count, fail_cap, mt, bm);
-    else if (sd.W == 64)
-        phase2_kernel<64, false><<<grid, 256, 0, st>>>(sd, algo, mode, split, fail_ids, fail_count, fail_cap, mt, bm);
-    else if (reg)
-        phase2_kernel<32, true><<<grid, 256, 0, st>>>(sd, algo, mode, split, fail_ids, fail_count, fail_cap, mt, bm);
-    else
-        phase2_kernel<32, false><<<grid, 256, 0, st>>>(sd, algo, mode, split, fail_ids, fail_count, fail_cap, mt, bm);
+    if (algo >= hrb::ALGO_REGULAR) {
+        const int g4 = sm_count() * HRB_P2_MINB * 4;  // grid-stride over failing domains (device count)
+        if (sd.W == 64) phase2_reg_kernel<64><<<g4, 128, 0, st>>>(sd, split, fail_ids, fail_t, fail_count, fail_cap, mt, bm);
+        else phase2_reg_kernel<32><<<g4, 128, 0, st>>>(sd, split, fail_ids, fail_t, fail_count, fail_cap, mt, bm);
+    } else {
+        if (sd.W == 64)
+            phase2_classic_kernel<64><<<grid, 256, 0, st>>>(sd, mode, split, fail_ids, fail_t, fail_count, fail_cap, mt, bm);
+        else
+            phase2_classic_kernel<32><<<grid, 256, 0, st>>>(sd, mode, split, fail_ids, fail_t, fail_count, fail_cap, mt, bm);
+    }
     CK(cudaGetLastError());
-    P2Compact fn{(const uint32_t*)ws.bm2.p, fail_ids, fail_count, fail_cap, (const unsigned long long*)ws.meta.p,
-                 sub_keys, cap};
+    P2Compact fn{(const uint32_t*)ws.bm2.p, fail_ids, fail_t, fail_count, fail_cap, mt, sub_keys,
+                 (uint32_t*)ws.sub_t.p, cap};
     return run_compact(ws, fn, sub_count, st);
 }
 
 int phase3_impl(Workspace& ws, const hrb_slice* s, const SliceDev& sd, int split, const uint64_t* sub_keys,
-                const uint64_t* sub_count, uint64_t sub_cap, uint64_t* cm, uint64_t* cd, uint64_t* cdom,
-                uint64_t* cand_count, uint64_t cap, cudaStream_t st) {
+                const uint32_t* sub_t, const uint64_t* sub_count, uint64_t sub_cap, uint64_t* cm, uint64_t* cd,
+                uint64_t* cdom, uint64_t* cand_count, uint64_t cap, cudaStream_t st) {
     int rc;
     const uint64_t maxstep = s->max_dom_n;  // >= every subdomain step
     const uint64_t CH = (maxstep + CHUNK3 - 1) / CHUNK3;
@@ -772,11 +1020,17 @@ int phase3_impl(Workspace& ws, const hrb_slice* s, const SliceDev& sd, int split
     const uint64_t app_cap = cap;
     if ((rc = ws.app.ensure(sizeof(Cand) * (app_cap + 1)))) return rc;
     if ((rc = ws.appc.ensure(sizeof(unsigned long long)))) return rc;
+    if (!sub_t) {
+        if ((rc = ws.sub_t.ensure(sizeof(uint32_t) * (sub_cap + 1)))) return rc;
+        locate_kernel<<<sm_count() * 4, 256, 0, st>>>(s->dom_base, sd.S, sub_keys, sub_count, sub_cap, 8,
+                                                      (uint32_t*)ws.sub_t.p);
+        sub_t = (const uint32_t*)ws.sub_t.p;
+    }
     CK(cudaMemsetAsync(ws.appc.p, 0, sizeof(unsigned long long), st));
     const int grid = sm_count() * 8;
-    phase3_kernel<<<grid, 256, 0, st>>>(sd, split, sub_keys, sub_count, sub_cap, (const unsigned long long*)ws.meta.p,
-                                        (uint32_t*)ws.counts3.p, (Cand*)ws.app.p, (unsigned long long*)ws.appc.p,
-                                        app_cap);
+    phase3_kernel<<<grid, 256, 0, st>>>(sd, split, sub_keys, sub_t, sub_count, sub_cap,
+                                        (const unsigned long long*)ws.meta.p, (uint32_t*)ws.counts3.p,
+                                        (Cand*)ws.app.p, (unsigned long long*)ws.appc.p, app_cap);
     CK(cudaGetLastError());
     P3Offsets fn{(const uint32_t*)ws.counts3.p, sub_count, sub_cap, (const unsigned long long*)ws.meta.p,
                  (uint64_t*)ws.offs3.p};
@@ -887,7 +1141,8 @@ int hrb_phase2(const hrb_slice* s, int algo, int mode, int split, const uint64_t
     if ((rc = current_ws(&ws))) return rc;
     SliceDev sd = to_dev(s);
     if ((rc = ws_prep(*ws, sd, split, st))) return rc;
-    return phase2_impl(*ws, s, sd, algo, mode, split, fail_ids, fail_count, fail_cap, sub_keys, sub_count, cap, st);
+    return phase2_impl(*ws, s, sd, algo, mode, split, fail_ids, nullptr, fail_count, fail_cap, sub_keys, sub_count,
+                       cap, st);
 }
 
 int hrb_phase3(const hrb_slice* s, int split, const uint64_t* sub_keys, const uint64_t* sub_count, uint64_t sub_cap,
@@ -902,7 +1157,8 @@ int hrb_phase3(const hrb_slice* s, int split, const uint64_t* sub_keys, const ui
     if ((rc = current_ws(&ws))) return rc;
     SliceDev sd = to_dev(s);
     if ((rc = ws_prep(*ws, sd, split, st))) return rc;
-    return phase3_impl(*ws, s, sd, split, sub_keys, sub_count, sub_cap, cand_index, cand_dist, cand_dom, cand_count,
+    return phase3_impl(*ws, s, sd, split, sub_keys, nullptr, sub_count, sub_cap, cand_index, cand_dist, cand_dom,
+                       cand_count,
                        cap, st);
 }
 
@@ -920,10 +1176,12 @@ int hrb_run_slice(const hrb_slice* s, int algo, int mode, int split, const hrb_r
     if ((rc = ws_prep(*ws, sd, split, st))) return rc;
     if ((rc = phase1_impl(*ws, s, sd, algo, mode, out->fail_ids, counts + 0, out->fail_cap, counts + 3, st)))
         return rc;
-    if ((rc = phase2_impl(*ws, s, sd, algo, mode, split, out->fail_ids, counts + 0, out->fail_cap, out->sub_keys,
+    if ((rc = phase2_impl(*ws, s, sd, algo, mode, split, out->fail_ids, (const uint32_t*)ws->fail_t.p, counts + 0,
+                          out->fail_cap, out->sub_keys,
                           counts + 1, out->sub_cap, st)))
         return rc;
-    return phase3_impl(*ws, s, sd, split, out->sub_keys, counts + 1, out->sub_cap, out->cand_index, out->cand_dist,
+    return phase3_impl(*ws, s, sd, split, out->sub_keys, (const uint32_t*)ws->sub_t.p, counts + 1, out->sub_cap,
+                       out->cand_index, out->cand_dist,
                        out->cand_dom, counts + 2, out->cand_cap, st);
 }
 
