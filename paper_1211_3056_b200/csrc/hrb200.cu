@@ -187,26 +187,34 @@ __device__ __forceinline__ hrb::Outcome search_one(int algo, int mode, const Pro
 // prep: tiles per super-domain, max subdomain count J, max subdomain step
 // ---------------------------------------------------------------------------
 __global__ void prep_kernel(SliceDev s, int split, uint64_t* tiles, unsigned long long* meta) {
-    int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (t > s.S) return;
-    if (t == s.S) {
-        tiles[t] = 0;
-        return;
-    }
-    uint32_t nd = s.n_dom[t];
-    tiles[t] = (nd + TILE - 1) / TILE;
-    uint64_t sizes[2] = {s.dom_n[t], s.last_n[t]};
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     unsigned long long J = 0, mstep = 0;
-    for (int k = 0; k < 2; k++) {
-        uint64_t n = sizes[k];
-        uint64_t step = n / split;
-        if (step < 1) step = 1;
-        uint64_t nsub = (n + step - 1) / step;
-        if (nsub > J) J = nsub;
-        if (step > mstep) mstep = step;
+    if (t < s.S) {
+        const uint32_t nd = s.n_dom[t];
+        tiles[t] = (nd + TILE - 1) / TILE;
+        const uint64_t sizes[2] = {s.dom_n[t], s.last_n[t]};
+        for (int k = 0; k < 2; k++) {
+            const uint64_t n = sizes[k];
+            uint64_t step = n / split;
+            if (step < 1) step = 1;
+            const uint64_t nsub = (n + step - 1) / step;
+            J = nsub > J ? nsub : J;
+            mstep = step > mstep ? step : mstep;
+        }
+    } else if (t == s.S) {
+        tiles[t] = 0;
     }
-    atomicMax(&meta[0], J);
-    atomicMax(&meta[1], mstep);
+    // one atomic per warp (65536 same-address atomics cost ~90 us)
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long j2 = __shfl_xor_sync(0xffffffffu, J, o);
+        const unsigned long long m2 = __shfl_xor_sync(0xffffffffu, mstep, o);
+        J = j2 > J ? j2 : J;
+        mstep = m2 > mstep ? m2 : mstep;
+    }
+    if ((threadIdx.x & 31) == 0 && J) {
+        atomicMax(&meta[0], J);
+        atomicMax(&meta[1], mstep);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -512,14 +520,51 @@ struct Cand {
     uint32_t rank;
 };
 
+// 96-bit lane registers for the phase-3 walk: value = (h << 64) + (m << 32),
+// the low 32 bits being the (zero) bits below the 2^-F grid once shifted by
+// sh = 128 - F >= 32.  V += D1 is one ALU add chain (IADD3 + 2 IADD3.X);
+// D1 += D2 is issued as IMAD-with-carry so it runs on the FMA pipe and the
+// two chains overlap (the walk is otherwise ALU-pipe bound).
+struct R96 {
+    uint32_t m;
+    uint64_t h;
+};
+
+__device__ __forceinline__ R96 r96_of(u128 x) {
+    R96 r;
+    r.m = (uint32_t)(x >> 32);
+    r.h = (uint64_t)(x >> 64);
+    return r;
+}
+
+__device__ __forceinline__ u128 u128_of(R96 r) { return ((u128)r.h << 64) | ((u128)r.m << 32); }
+
+__device__ __forceinline__ void add96_alu(R96& x, const R96& y) {
+    uint32_t h0 = (uint32_t)x.h, h1 = (uint32_t)(x.h >> 32);
+    asm("add.cc.u32 %0, %0, %3;\n\taddc.cc.u32 %1, %1, %4;\n\taddc.u32 %2, %2, %5;"
+        : "+r"(x.m), "+r"(h0), "+r"(h1)
+        : "r"(y.m), "r"((uint32_t)y.h), "r"((uint32_t)(y.h >> 32)));
+    x.h = ((uint64_t)h1 << 32) | h0;
+}
+
+__device__ __forceinline__ void add96_fma(R96& x, const R96& y) {
+    uint32_t h0 = (uint32_t)x.h, h1 = (uint32_t)(x.h >> 32);
+    asm("mad.lo.cc.u32 %0, %3, 1, %0;\n\tmadc.lo.cc.u32 %1, %4, 1, %1;\n\tmadc.lo.u32 %2, %5, 1, %2;"
+        : "+r"(x.m), "+r"(h0), "+r"(h1)
+        : "r"(y.m), "r"((uint32_t)y.h), "r"((uint32_t)(y.h >> 32)));
+    x.h = ((uint64_t)h1 << 32) | h0;
+}
+
 // Phase 3 walk, scaled form: with sh = 128 - F the registers hold
 // V = (v + window - 1) 2^sh, D1 = d1 2^sh, D2 = d2 2^sh, so the mod-2^F
 // walk of pipeline.py:291-292 is plain 128-bit wraparound and the
 // two-sided window test of pipeline.py:281 (v < window or v > 2^F - window)
 // is the single unsigned compare V < (2 window - 1) 2^sh.  Hits are rare
-// (~2 eps' per argument): a lane ORs its hits over 32 arguments, and only
-// when some lane of the warp hit does the warp re-walk those 32 arguments
-// and append the candidates with __ballot_sync/__popc (one atomic per warp).
+// (~2 eps' per argument): the hot loop only ORs a conservative test on the
+// top 64 bits over 32 arguments; when some lane of the warp flagged, the
+// warp re-walks those 32 arguments exactly and appends the candidates with
+// __ballot_sync/__popc (one atomic per warp).
+template <bool NARROW>
 __global__ void __launch_bounds__(256) phase3_kernel(SliceDev s, int split, const uint64_t* sub_keys,
                                                      const uint32_t* sub_t, const uint64_t* sub_count,
                                                      uint64_t sub_cap, const unsigned long long* meta,
@@ -569,17 +614,25 @@ __global__ void __launch_bounds__(256) phase3_kernel(SliceDev s, int split, cons
                 mbase = __ldg(&s.m0[t]) + i * (uint64_t)__ldg(&s.dom_n[t]) + o;
             }
         }
+        const uint64_t Khi = (uint64_t)(K >> 64);
         uint32_t rank = 0;
+        R96 v96 = r96_of(V), d96 = r96_of(D1), e96 = r96_of(D2);
         for (uint32_t x0 = 0; x0 < CHUNK3; x0 += 32) {
-            const u128 V0 = V, D10 = D1;
+            const u128 V0 = NARROW ? u128_of(v96) : V, D10 = NARROW ? u128_of(d96) : D1;
             bool any = false;
-#pragma unroll 8
+#pragma unroll 16
             for (uint32_t x = 0; x < 32; x++) {
-                any |= (x0 + x < len) && V < K;
-                V += D1;
-                D1 += D2;
+                if (NARROW) {
+                    any |= v96.h <= Khi;  // conservative: V < K implies hi(V) <= hi(K)
+                    add96_alu(v96, d96);
+                    add96_fma(d96, e96);
+                } else {
+                    any |= (uint64_t)(V >> 64) <= Khi;
+                    V += D1;
+                    D1 += D2;
+                }
             }
-            if (__any_sync(0xffffffffu, any)) {  // rare: re-walk and append in order
+            if (__any_sync(0xffffffffu, any)) {  // rare: re-walk exactly and append in order
                 u128 v = V0, d = D10;
                 for (uint32_t x = 0; x < 32; x++) {
                     const bool hit = (x0 + x < len) && v < K;
@@ -1028,9 +1081,14 @@ int phase3_impl(Workspace& ws, const hrb_slice* s, const SliceDev& sd, int split
     }
     CK(cudaMemsetAsync(ws.appc.p, 0, sizeof(unsigned long long), st));
     const int grid = sm_count() * 8;
-    phase3_kernel<<<grid, 256, 0, st>>>(sd, split, sub_keys, sub_t, sub_count, sub_cap,
-                                        (const unsigned long long*)ws.meta.p, (uint32_t*)ws.counts3.p,
-                                        (Cand*)ws.app.p, (unsigned long long*)ws.appc.p, app_cap);
+    if (sd.F <= 96)
+        phase3_kernel<true><<<grid, 256, 0, st>>>(sd, split, sub_keys, sub_t, sub_count, sub_cap,
+                                                  (const unsigned long long*)ws.meta.p, (uint32_t*)ws.counts3.p,
+                                                  (Cand*)ws.app.p, (unsigned long long*)ws.appc.p, app_cap);
+    else
+        phase3_kernel<false><<<grid, 256, 0, st>>>(sd, split, sub_keys, sub_t, sub_count, sub_cap,
+                                                   (const unsigned long long*)ws.meta.p, (uint32_t*)ws.counts3.p,
+                                                   (Cand*)ws.app.p, (unsigned long long*)ws.appc.p, app_cap);
     CK(cudaGetLastError());
     P3Offsets fn{(const uint32_t*)ws.counts3.p, sub_count, sub_cap, (const unsigned long long*)ws.meta.p,
                  (uint64_t*)ws.offs3.p};

@@ -32,34 +32,60 @@ __device__ __forceinline__ double rcp_refined(double xd) {
 // one search in flight, role form (see search_core.cuh RegState)
 struct Slot {
     uint64_t S, L, d;
-    double Sd, Ld;
-    uint32_t cS, cL, it;
+    float Sf, Lf;  // S, L rounded to float: only ever used for quotient estimates
+    uint32_t cS, cL;
 };
+
+// Quotient estimate from the FP32 reciprocal: with M = 1.5 * 2^23 the FFMA
+// y*rcp(x) + (M - 1) lands in [2^23, 2^24) where floats are the integers, so
+// its single rounding IS round-to-nearest(y/x - 1 + e) with |e| < 2^-22 y/x;
+// for y/x < 2^20 that is floor(y/x) or floor(y/x) - 1 (possibly -1 when the
+// quotient is 0), read straight from the bit pattern -- no F2I on the
+// conversion pipe.  Quotients >= 2^20 are reported for the exact path.
+__device__ __forceinline__ int32_t qest(float yf, float rcp) {
+    const float kf = fmaf(yf, rcp, 12582911.0f);  // 1.5 * 2^23 - 1
+    return (int32_t)(__float_as_uint(kf) - 0x4B400000u);
+}
+
+// r = y - k x with k in {K-1, K} (K = floor(y/x)), fixed to the exact
+// remainder; returns the exact quotient.  k = -1 (K = 0) is clamped to 0,
+// where y < x already holds, so the products stay unsigned 32x64.
+__device__ __forceinline__ uint32_t qfix(uint64_t y, uint64_t x, int32_t k, uint64_t& r) {
+    const uint32_t ku = (uint32_t)max(k, 0);
+    const uint64_t rr = y - (uint64_t)ku * x;
+    const bool c = rr >= x;
+    r = c ? rr - x : rr;
+    return ku + (c ? 1u : 0u);
+}
+
+__device__ __forceinline__ float rcp_approx(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));  // <= 1 ulp
+    return r;
+}
+
+constexpr int32_t QMAX = 1 << 20;
 
 // One half-step; THEN selects the reference's `p < q` body (d %= p) versus
 // the `p >= q` body (d reduced past the new p).  Returns true when the
-// search ended (verdict d > eps, iterations s.it); the state is advanced
-// unconditionally, so a finished slot keeps computing harmless garbage.
+// search ended (verdict d > eps); the state is advanced unconditionally, so
+// a finished slot keeps computing harmless garbage.  Invariant S <= 2^63
+// (S is a remainder of 2^W by a, or smaller).
 template <bool THEN>
 __device__ __forceinline__ bool half_step(Slot& s, uint32_t N) {
     const uint64_t S = s.S, L = s.L;
-    const double inv = rcp_refined(s.Sd);
-    // quotient of the continued fraction: estimate, then one fix-up
-    const double kd = fma(s.Ld, inv, -0.5);
-    uint32_t k = __double2uint_rz(kd);
-    uint64_t Lp = L - (uint64_t)k * S;
-    const bool c = Lp >= S;
-    Lp = c ? Lp - S : Lp;
-    k += c ? 1u : 0u;
+    const float rcp = rcp_approx(s.Sf);
+    const int32_t ke = qest(s.Lf, rcp);
+    uint64_t Lp;
+    const uint32_t k = qfix(L, S, ke, Lp);
     uint64_t cLp = (uint64_t)k * s.cS + s.cL;
     // d reduction: then-body d mod S; else-body (d >= Lp ? d - Lp : d) mod S
     // (when d < Lp, d < S already and the mod is the identity)
     uint64_t x = (!THEN && s.d >= Lp) ? s.d - Lp : s.d;
-    const double kd2 = fma(__ull2double_rn(x), inv, -0.5);
-    const uint32_t k2 = __double2uint_rz(kd2);
-    uint64_t dn = x - (uint64_t)k2 * S;
-    dn = dn >= S ? dn - S : dn;
-    if (!(fmax(kd, kd2) < TWO32)) {  // rare: a quotient >= 2^32 (exact path)
+    const int32_t ke2 = qest(__ull2float_rn(x), rcp);
+    uint64_t dn;
+    qfix(x, S, ke2, dn);
+    if (ke >= QMAX || ke2 >= QMAX) {  // rare: a quotient >= 2^20 (exact path)
         const uint64_t kk = S ? L / S : 0;
         Lp = L - kk * S;
         cLp = kk * (uint64_t)s.cS + s.cL;  // true value <= 2^64; == 2^64 only if Lp == 0 and S == 1
@@ -67,12 +93,11 @@ __device__ __forceinline__ bool half_step(Slot& s, uint32_t N) {
         dn = S ? x % S : x;
     }
     s.d = dn;
-    s.it++;
     const bool done = Lp == 0 || cLp >= (uint64_t)(N - s.cS);
     s.L = S;
-    s.Ld = s.Sd;
+    s.Lf = s.Sf;
     s.S = Lp;
-    s.Sd = __ull2double_rn(Lp);
+    s.Sf = __ull2float_rn(Lp);
     s.cL = s.cS;
     s.cS = (uint32_t)cLp;
     return done;
@@ -138,11 +163,10 @@ __device__ __forceinline__ bool reg_start(uint64_t a, uint64_t b, uint64_t eps, 
     s.S = rem;
     s.L = a;
     s.d = d;
-    s.Sd = __ull2double_rn(rem);
-    s.Ld = ad;
+    s.Sf = __ull2float_rn(rem);
+    s.Lf = __ull2float_rn(a);
     s.cS = (uint32_t)k;
     s.cL = 1;
-    s.it = 1;
     return false;
 }
 
@@ -186,28 +210,31 @@ __device__ __forceinline__ uint32_t lane_items(Src& src, unsigned long long* ite
             s1 = s0;
             n1 = n0;
         }
+        uint32_t h = 1;  // half-steps so far (both slots start after their first then-half)
         while (act0 || act1) {
             bool f0 = half_step<false>(s0, n0);
             bool f1 = half_step<false>(s1, n1);
+            h++;
             if (act0 && f0) {
-                its += halve ? (s0.it + 1) >> 1 : s0.it;
+                its += halve ? (h + 1) >> 1 : h;
                 fails |= (s0.d > e0) ? 0u : 1u << k;
                 act0 = false;
             }
             if (act1 && f1) {
-                its += halve ? (s1.it + 1) >> 1 : s1.it;
+                its += halve ? (h + 1) >> 1 : h;
                 fails |= (s1.d > e1) ? 0u : 2u << k;
                 act1 = false;
             }
             f0 = half_step<true>(s0, n0);
             f1 = half_step<true>(s1, n1);
+            h++;
             if (act0 && f0) {
-                its += halve ? (s0.it + 1) >> 1 : s0.it;
+                its += halve ? (h + 1) >> 1 : h;
                 fails |= (s0.d > e0) ? 0u : 1u << k;
                 act0 = false;
             }
             if (act1 && f1) {
-                its += halve ? (s1.it + 1) >> 1 : s1.it;
+                its += halve ? (h + 1) >> 1 : h;
                 fails |= (s1.d > e1) ? 0u : 2u << k;
                 act1 = false;
             }
