@@ -20,7 +20,8 @@ CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(LIBDIR, "libhrb200.so")
 SOURCES = [os.path.join(CSRC, "hrb200.cu")]
-HEADERS = [os.path.join(CSRC, "search_core.cuh"), os.path.join(ROOT, "include", "hrb200.h")]
+HEADERS = [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC)) if f.endswith((".cuh", ".h"))] + [
+    os.path.join(ROOT, "include", "hrb200.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
