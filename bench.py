@@ -1,14 +1,16 @@
 """Benchmark: binary64 exp HR search, args tested/sec (BASELINE.json metric).
 
 Workload (BASELINE.json configs[2]): exp over binade [1,2)
-of binary64, 2^40 consecutive arguments per GPU (weak scaling: rank r owns
-indices [r 2^40, (r+1) 2^40)), domains of N = 2^15 arguments, super-domains
-of 2^24 arguments (tau = 512 Taylor blocks, delta = 2, F = 96, L = 8),
-eps = 2^-32, regular search, phase-2 split 8.  One step = the whole device
-hot path over the slice (tabulated walk + Boolean tests + search +
-compaction, phase 2, phase 3, ordered candidate output): hrb_run_slice.
-The host Taylor generation (mpmath, reused unchanged from the paper's
-hybrid split) runs once before timing; its rate is reported separately.
+of binary64, 2^40 consecutive arguments per GPU (weak scaling: the range
+[0, N_gpus 2^40) is cut into contiguous runs of 2^24-argument super-domain
+blocks, one run per rank, shard.partition_blocks), domains of N = 2^15
+arguments, super-domains of 2^24 arguments (tau = 512 Taylor blocks,
+delta = 2, F = 96, L = 8), eps = 2^-32, regular search, phase-2 split 8.
+One step = the whole device hot path over the rank's slice (tabulated walk
++ Boolean tests + search + compaction, phase 2, phase 3, ordered candidate
+output): one hrb_run_slice.  The host Taylor generation (mpmath, kept on
+the host as in the paper's hybrid split) runs once before timing; its rate
+is reported separately under host_polygen.
 
     python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
@@ -18,6 +20,7 @@ Prints one JSON line on rank 0.
 from __future__ import annotations
 
 import argparse
+import ctypes as C
 import json
 import os
 import subprocess
@@ -32,7 +35,9 @@ sys.path.insert(0, ROOT)
 
 METRIC = "binary64 args tested/sec (exp) at 1/2/4/8 B200 vs CPU ref; % of INT-pipe peak"
 UNIT = "args/s"
-KERNELS_PER_STEP = 16  # prep, 2 scan, phase1, 3 compact, phase2, 3 compact, phase3, 3 scan, scatter
+# kernels per hrb_run_slice: prep, cub scan (2), phase1 + 3 compaction, phase2 + 3, phase3 + 3 + scatter
+KERNELS_PER_STEP = 16
+CALIBRATION = os.path.join(ROOT, "profiles", "calibration.json")
 
 
 def parse():
@@ -41,12 +46,12 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--log2-args", type=int, default=40)
+    ap.add_argument("--log2-args", type=int, default=40, help="arguments per GPU (log2)")
     ap.add_argument("--eps-bits", type=int, default=32)
     ap.add_argument("--algo", default="regular", choices=("regular", "lefevre"))
     ap.add_argument("--log2-super", type=int, default=24)
     ap.add_argument("--log2-N", type=int, default=15)
-    ap.add_argument("--cpu-sample-log2", type=int, default=36, help="arguments in the CPU-baseline sample")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0, help="minimum CPU-baseline timing window")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -69,12 +74,23 @@ def make_cfg(args):
     return PipelineConfig("exp", FpFormat(53, args.eps_bits), pg, PhaseConfig(args.algo, phase2_split=8, N1=N))
 
 
-def prepare(args, start, count, workers):
-    from paper_1211_3056_b200.funnel import prepare_slice
+def prepare_rank(args, rank, world, workers):
+    """The rank's contiguous share of [0, world 2^log2_args), packed."""
+    from paper_1211_3056_b200.shard import partition_blocks
+    from paper_1211_3056_b200.slices import pack_slice, plan_blocks, supers_of_blocks
 
+    cfg = make_cfg(args)
     t0 = time.perf_counter()
-    batch = prepare_slice("exp", 0, start, count, make_cfg(args), workers=workers)
+    blocks = plan_blocks("exp", 0, cfg.fmt, cfg.polygen, 0, world << args.log2_args)
+    b0, b1 = partition_blocks([b.bcount for b in blocks], world)[rank]
+    supers = supers_of_blocks(blocks[b0:b1], workers)
+    batch = pack_slice(supers, cfg.fmt, cfg.polygen, cfg.word_bits, 0)
     return batch, time.perf_counter() - t0
+
+
+def workload_name(args):
+    return (f"exp p=53 [1,2) 2^{args.log2_args} args/GPU eps=2^-{args.eps_bits} N=2^{args.log2_N} "
+            f"super=2^{args.log2_super} delta=2 F=96 W=64 split=8 {args.algo}")
 
 
 class ClockSampler:
@@ -99,7 +115,7 @@ class ClockSampler:
                     self.samples.append(vals)
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.05)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -122,59 +138,85 @@ class ClockSampler:
 
 
 def load_calibration():
-    p = os.path.join(ROOT, "profiles", "calibration.json")
-    if os.path.exists(p):
-        with open(p) as fh:
+    if os.path.exists(CALIBRATION):
+        with open(CALIBRATION) as fh:
             return json.load(fh)
     return {}
 
 
-def cpu_baseline(args, sample_log2: int):
-    """The oracle port (oracle/hr_oracle.c, OpenMP over all host threads)
-    timed on a bounded contiguous sample of the same workload."""
+def oracle_funnel(batch, algo):
+    """Phases 1-3 of the CPU oracle port (OpenMP over all host threads)."""
+    import oracle
+
+    fails = oracle.phase1(batch, algo, 1)
+    rows = oracle.phase2(batch, algo, 1, 8, fails)
+    m, _, _ = oracle.phase3(batch, rows)
+    return len(fails), len(rows[0]), len(m)
+
+
+def cpu_baseline(args, batch, min_seconds):
+    """The oracle port (oracle/hr_oracle.c) timed on the SAME packed slice
+    (the full per-GPU workload) on this box's host cores, repeated until
+    `min_seconds` of CPU time have elapsed; also checks its counts."""
     import oracle
 
     oracle.build()
-    count = 1 << sample_log2
-    batch, _ = prepare(args, 0, count, os.cpu_count() or 1)
-    threads = oracle.threads()
-    t0 = time.perf_counter()
-    fails = oracle.phase1(batch, args.algo, 1)
-    rows = oracle.phase2(batch, args.algo, 1, 8, fails)
-    oracle.phase3(batch, rows)
-    dt = time.perf_counter() - t0
-    return {"value": count / dt, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"exp p=53 indices [0, 2^{sample_log2}) (same config), phases 1-3, {dt:.2f} s"}
+    times, counts = [], None
+    t_end = time.perf_counter() + min_seconds
+    while not times or time.perf_counter() < t_end:
+        t0 = time.perf_counter()
+        counts = oracle_funnel(batch, args.algo)
+        times.append(time.perf_counter() - t0)
+    dt = float(np.mean(times))
+    return {"value": batch.arguments / dt, "unit": UNIT, "cores": oracle.threads(), "kind": "port",
+            "sample": f"the full per-GPU workload ({workload_name(args)}), phases 1-3, {len(times)} runs x "
+                      f"{dt:.2f} s (same packed slice as the GPU)", "counts": list(counts)}
 
 
 def run_reference(args):
+    """--impl reference: the reference path on the host cores (oracle port
+    of the reference's CPU algorithm), same config and metric."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
     import oracle
 
     oracle.build()
-    count = 1 << args.cpu_sample_log2
-    batch, _ = prepare(args, 0, count, os.cpu_count() or 1)
+    workers = os.cpu_count() or 1
+    batch, _ = prepare_rank(args, 0, 1, workers)
     times = []
     for k in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        fails = oracle.phase1(batch, args.algo, 1)
-        rows = oracle.phase2(batch, args.algo, 1, 8, fails)
-        oracle.phase3(batch, rows)
+        oracle_funnel(batch, args.algo)
         if k >= args.warmup:
             times.append(time.perf_counter() - t0)
-    v = count / float(np.mean(times))
+    ms = 1e3 * float(np.mean(times))
+    v = batch.arguments / (ms / 1e3)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(times)),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64",
             "data": "synthetic: exp binade [1,2) argument range (real Taylor blocks)",
-            "config": {"workload": f"exp p=53 eps=2^-{args.eps_bits} N=2^{args.log2_N} CPU sample 2^{args.cpu_sample_log2} "
-                                   f"args (of the 2^{args.log2_args}/GPU slice)", "algo": args.algo},
+            "config": {"workload": workload_name(args), "parallelism": "host threads (OpenMP)"},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": oracle.threads(), "kind": "port",
-                             "sample": f"indices [0, 2^{args.cpu_sample_log2}), phases 1-3 per step"},
+                             "sample": f"the full per-GPU workload, phases 1-3, {args.steps} timed runs"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def int_peak():
+    """Measured INT-pipe issue peak (lane-ops/s) of this device: IADD3 + IMAD
+    chains, and IADD3 alone (csrc/intpeak.cu)."""
+    from paper_1211_3056_b200.build import PEAK_LIB
+
+    lib = C.CDLL(PEAK_LIB)
+    lib.hrb_int_peak.argtypes = [C.c_int, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_float)]
+    out = {}
+    for mix, key in ((1, "alu_fma"), (0, "alu_only")):
+        v, ms = C.c_double(0), C.c_float(0)
+        if lib.hrb_int_peak(mix, 5, C.byref(v), C.byref(ms)) != 0:
+            raise RuntimeError("hrb_int_peak failed")
+        out[key] = v.value
+    return out
 
 
 def main():
@@ -185,7 +227,8 @@ def main():
     rank, world, local = dist_env()
     import torch
 
-    from paper_1211_3056_b200.device import DeviceSlice, FusedRunner, run_host
+    from paper_1211_3056_b200 import _native as nat
+    from paper_1211_3056_b200.device import DeviceSlice, FusedRunner, HostRunner, run_phases
 
     torch.cuda.set_device(local)
     dist = None
@@ -193,27 +236,25 @@ def main():
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    count = 1 << args.log2_args
     workers = max(1, (os.cpu_count() or 1) // max(1, int(os.environ.get("LOCAL_WORLD_SIZE", world))))
-    batch, prep_s = prepare(args, rank * count, count, workers)
+    batch, prep_s = prepare_rank(args, rank, world, workers)
+    count = batch.arguments
     algo = 2 if args.algo == "regular" else 0
     ds = DeviceSlice(batch)
     sub_cap = max(1 << 16, batch.n_total * 2)
     runner = FusedRunner(ds, algo, 1, 8, sub_cap=sub_cap, cand_cap=1 << 20)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
     stream = torch.cuda.current_stream()
-    for _ in range(args.warmup):
+    for _ in range(max(3, args.warmup)):
         runner.launch()
     torch.cuda.synchronize()
     counts0 = runner.counts_host().copy()
-    # phase-1 kernel alone, for the roofline (same stream, CUDA events)
-    from paper_1211_3056_b200 import _native as nat
-    import ctypes as C
-
     lib = nat.load()
+    # phase-1 kernel + its compaction alone (the dominant kernel), CUDA events
+    # on the launching stream, L2 flushed before each launch
     p1_ms = []
     cnt = ds.empty64(4)
-    for _ in range(max(3, args.steps // 2)):
+    for _ in range(max(5, args.steps)):
         cnt.zero_()
         flush.zero_()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -224,13 +265,11 @@ def main():
         torch.cuda.synchronize()
         p1_ms.append(e0.elapsed_time(e1))
     iters = int(cnt.cpu().numpy().view(np.uint64)[3])
-    from paper_1211_3056_b200.device import run_phases
-
-    phase_ms = [0.0, 0.0, 0.0]
+    phase_ms = None
     for _ in range(3):
         r = run_phases(ds, algo, 1, 8, cand_hint=1 << 20)
-        phase_ms = [min(a, b) if phase_ms[0] else b for a, b in zip(phase_ms, r.phase_ms)]
-    # timed region
+        phase_ms = list(r.phase_ms) if phase_ms is None else [min(a, b) for a, b in zip(phase_ms, r.phase_ms)]
+    # ---- timed region: K steps, L2 flushed between steps, events on the stream
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     sampler = ClockSampler(local)
     if dist:
@@ -249,73 +288,90 @@ def main():
     ms = float(np.mean(step_ms))
     counts = runner.counts_host().copy()
     assert np.array_equal(counts, counts0), "non-deterministic counts across steps"
-    # e2e: the C-ABI host-buffer entry point (H2D of the packed slice, all
-    # kernels, D2H of counts + failing ids + candidates), wall clock
+    # ---- e2e: the C-ABI host-buffer entry point (H2D of the packed slice from
+    # pinned memory, all kernels, D2H of counts + failing ids + candidates)
     e2e = None
     if not args.no_e2e:
-        pinned = {}
-        for name in ("coef", "G", "s2abs", "n_dom", "dom_n", "last_n", "dom_base", "m0"):
-            arr = getattr(batch, name)
-            t = torch.from_numpy(arr.view(np.int32 if arr.dtype == np.uint32 else np.int64)).pin_memory()
-            pinned[name] = t
-            setattr(batch, name, t.numpy().view(arr.dtype))
-        run_host(batch, algo, 1, 8)
+        host = HostRunner(batch, algo, 1, 8)
+        host.run()
         e2e_t = []
-        for _ in range(max(2, args.steps // 2)):
+        for _ in range(max(3, args.steps // 2)):
+            if dist:
+                dist.barrier()
             t0 = time.perf_counter()
-            hc, hf, hm, hd, hdom, _ = run_host(batch, algo, 1, 8)
+            hc, hf, hm, hd, hdom = host.run()
             e2e_t.append(time.perf_counter() - t0)
+        assert np.array_equal(hc, counts), "host-buffer path disagrees with the device path"
         e2e_ms = 1e3 * float(np.mean(e2e_t))
-        h2d = batch.nbytes()
-        d2h = 32 + 8 * int(hc[0]) + 24 * int(hc[2])
-        e2e = {"value": count * world / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms}
-    # max over ranks
-    t_all = torch.tensor([ms, float(np.mean(p1_ms))], device="cuda")
+        e2e = {"value": None, "unit": UNIT, "h2d_bytes_per_step": host.input_bytes(),
+               "d2h_bytes_per_step": host.output_bytes(), "ms_per_step": e2e_ms}
+    # ---- end of run: NCCL gather of the per-rank counters and candidate lists
+    from paper_1211_3056_b200.fpformat import index_bits
+    from paper_1211_3056_b200.shard import ShardResult, gather_shards
+
+    res = runner.result()
+    bits = [index_bits(0, int(m), batch.fmt) for m in res.cand_index.tolist()]
+    cand = np.array([[b >> 64, b & ((1 << 64) - 1), int(d), batch.id0 + int(i)]
+                     for b, d, i in zip(bits, res.cand_dist.tolist(), res.cand_dom.tolist())],
+                    dtype=np.uint64).reshape(-1, 4)
+    local_res = ShardResult(np.array([counts[0], counts[1], counts[2], 0, counts[3], count], dtype=np.int64), cand)
+    t_all = torch.tensor([ms, float(np.mean(p1_ms)), e2e["ms_per_step"] if e2e else 0.0], device="cuda")
+    gather_ms = 0.0
     if dist:
         dist.all_reduce(t_all, op=dist.ReduceOp.MAX)
-        allc = torch.tensor(counts.astype(np.int64), device="cuda")
-        dist.all_reduce(allc)  # end-of-run gather of the per-rank counters (NCCL)
-        tot_counts = allc.cpu().numpy()
+        torch.cuda.synchronize()
+        tg = time.perf_counter()
+        merged, per_rank = gather_shards(local_res)
+        gather_ms = 1e3 * (time.perf_counter() - tg)
     else:
-        tot_counts = counts.astype(np.int64)
-    ms_max, p1_max = float(t_all[0]), float(t_all[1])
+        merged, per_rank = local_res, local_res.counters[None, :]
+    ms_max, p1_max, e2e_max = (float(x) for x in t_all.cpu())
     if rank != 0:
-        if dist:
-            dist.destroy_process_group()
+        dist.destroy_process_group()
         return
-    value = count * world / (ms_max / 1e3)
+    total_args = int(per_rank[:, 5].sum())
+    value = total_args / (ms_max / 1e3)
+    if e2e:
+        e2e["value"] = total_args / (e2e_max / 1e3)
+        e2e["ms_per_step"] = e2e_max
     clocks = sampler.summary()
+    # ---- roofline of the dominant kernel (phase 1): INT-pipe bound
+    peak = int_peak()
     calib = load_calibration()
-    instr_per_step = calib.get("phase1_int_lane_instr_per_step")
-    sm_mhz = clocks.get("sm_mhz") or 1965.0
-    peak_tops = 148 * 128 * sm_mhz * 1e6 / 1e12  # alu + fma pipes: 1 warp-instr/clk/SMSP
-    achieved = (iters * instr_per_step / (p1_max / 1e3) / 1e12) if instr_per_step else None
-    roofline = {"bound": "int", "kernel": "phase1_kernel", "unit": "Tops/s",
-                "achieved": achieved, "peak": peak_tops,
-                "peak_basis": "148 SM x 128 INT lanes/clk (alu+fma pipes) x median SM clock under load",
-                "frac": (achieved / peak_tops) if achieved else None,
-                "traffic": calib.get("phase1_dram_bytes_per_launch"),
-                "quotient_steps_per_launch": iters, "phase1_ms": p1_max,
-                "steps_per_s": iters / (p1_max / 1e3),
-                "int_lane_instr_per_step": instr_per_step,
+    k1 = calib.get("phase1_reg_kernel", {})
+    lane_per_step = k1.get("int_lane_instr_per_quotient_step")
+    achieved = iters * lane_per_step / (p1_max / 1e3) if lane_per_step else None
+    roofline = {"bound": "int", "kernel": "phase1_reg_kernel (+ ordered compaction)", "unit": "Tops/s",
+                "achieved": achieved / 1e12 if achieved else None, "peak": peak["alu_fma"] / 1e12,
+                "peak_basis": "measured: IADD3+IMAD dependency chains on all SMs (csrc/intpeak.cu), lane-ops/s",
+                "frac": achieved / peak["alu_fma"] if achieved else None,
+                "alu_only_peak": peak["alu_only"] / 1e12,
+                "traffic": k1.get("dram_bytes_per_launch"),
+                "algorithmic_unit": "CF quotient step (SearchOutcome.iterations)",
+                "quotient_steps_per_launch": iters, "kernel_ms": p1_max,
+                "quotient_steps_per_s": iters / (p1_max / 1e3),
+                "int_lane_instr_per_quotient_step": lane_per_step,
+                "calibration": os.path.relpath(CALIBRATION, ROOT) if k1 else None,
                 "phase_ms_incl_compaction": phase_ms}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u64",
             "data": "synthetic: exp binade [1,2) argument ranges, Taylor blocks generated on the host (mpmath)",
-            "config": {"workload": f"exp p=53 2^{args.log2_args} args/GPU eps=2^-{args.eps_bits} "
-                                   f"N=2^{args.log2_N} super=2^{args.log2_super} delta=2 F=96 split=8 {args.algo}",
-                       "parallelism": f"shard{world} (contiguous argument blocks, no collective on the hot path)",
+            "config": {"workload": workload_name(args),
+                       "parallelism": f"shard{world} (contiguous super-domain blocks, no collective on the hot path; "
+                                      f"NCCL gather of counters + candidates at the end)",
                        "l2": "flushed between steps (256 MiB write)",
-                       "domains_per_gpu": batch.n_total, "phase1_fail": int(tot_counts[0]),
-                       "phase2_survivors": int(tot_counts[1]), "candidates": int(tot_counts[2])},
+                       "domains_per_gpu": batch.n_total, "phase1_fail": int(merged.counters[0]),
+                       "phase2_survivors": int(merged.counters[1]), "candidates": int(merged.counters[2]),
+                       "gather_ms": gather_ms},
             "clocks": clocks, "gpu_launches": KERNELS_PER_STEP * args.steps, "roofline": roofline,
             "host_polygen": {"seconds": prep_s, "workers": workers, "super_domains": batch.n_super,
                              "args_per_s": count / prep_s},
             "e2e": e2e}
     if not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(args, args.cpu_sample_log2)
+        cb = cpu_baseline(args, batch, args.cpu_seconds)
+        cb["counts_match_gpu"] = cb.pop("counts") == [int(counts[0]), int(counts[1]), int(counts[2])]
+        line["cpu_baseline"] = cb
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()

@@ -19,7 +19,9 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(LIBDIR, "libhrb200.so")
+PEAK_LIB = os.path.join(LIBDIR, "libhrbpeak.so")  # INT-pipe microbenchmark (roofline denominator)
 SOURCES = [os.path.join(CSRC, "hrb200.cu")]
+PEAK_SOURCES = [os.path.join(CSRC, "intpeak.cu")]
 HEADERS = [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC)) if f.endswith((".cuh", ".h"))] + [
     os.path.join(ROOT, "include", "hrb200.h")]
 
@@ -38,27 +40,33 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found: the CUDA toolkit is required to build libhrb200.so")
 
 
-def _stale() -> bool:
-    if not os.path.exists(LIB):
+def _stale(lib: str, sources: list) -> bool:
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
-    return any(os.path.getmtime(p) > t for p in SOURCES + HEADERS)
+    t = os.path.getmtime(lib)
+    return any(os.path.getmtime(p) > t for p in sources + HEADERS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    """Compile libhrb200.so for sm_100a if missing or stale; return its path."""
-    if not force and not _stale():
-        return LIB
+def _compile(lib: str, sources: list, verbose: bool) -> None:
     os.makedirs(LIBDIR, exist_ok=True)
-    tmp = LIB + ".tmp"
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", tmp, *SOURCES]
+    tmp = lib + ".tmp"
+    cmd = [nvcc(), *NVCC_FLAGS, "-o", tmp, *sources]
     proc = subprocess.run(cmd, capture_output=True, text=True)
     if proc.returncode != 0:
         sys.stderr.write(proc.stdout + proc.stderr)
         raise RuntimeError(f"nvcc failed ({proc.returncode}): {' '.join(cmd)}")
     if verbose:
         sys.stderr.write(proc.stderr)
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile libhrb200.so (and the INT-peak probe libhrbpeak.so) for
+    sm_100a if missing or stale; return the main library's path."""
+    if force or _stale(LIB, SOURCES):
+        _compile(LIB, SOURCES, verbose)
+    if force or _stale(PEAK_LIB, PEAK_SOURCES):
+        _compile(PEAK_LIB, PEAK_SOURCES, verbose)
     return LIB
 
 

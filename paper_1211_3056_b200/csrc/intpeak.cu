@@ -1,0 +1,86 @@
+// intpeak.cu -- measured INT-pipe peak of the device (roofline denominator).
+//
+// Not part of the C-ABI of include/hrb200.h: a measurement tool that bench.py
+// loads beside it.  Every thread runs 8 independent dependency chains of
+// 32-bit integer adds (IADD3, ALU pipe) and 8 of integer multiply-adds
+// (IMAD, FMA pipe), interleaved, so the SM sub-partition schedulers can
+// issue one integer warp-instruction per clock (the issue limit).  The
+// returned figure is lane-ops/s = warp-instructions * 32 / seconds, the same
+// unit the HR kernels' achieved INT throughput is quoted in.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace {
+
+template <int REPS, bool MIX>
+__global__ void __launch_bounds__(256) int_peak_kernel(uint32_t seed, uint32_t* sink) {
+    uint32_t a[8], m[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        a[k] = seed + threadIdx.x * 7u + k;
+        m[k] = seed ^ (threadIdx.x + 13u * k);
+    }
+    const uint32_t c = seed | 1u;
+#pragma unroll 8
+    for (int r = 0; r < REPS; r++) {
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            // IADD3 on the ALU pipe
+            asm volatile("add.u32 %0, %0, %1;" : "+r"(a[k]) : "r"(c));
+            // IMAD on the FMA pipe (mix == 0: ALU only)
+            if (MIX) asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(m[k]) : "r"(c), "r"(a[k]));
+        }
+    }
+    uint32_t x = 0;
+#pragma unroll
+    for (int k = 0; k < 8; k++) x ^= a[k] ^ m[k];
+    if (x == 0x9E3779B9u) sink[0] = x;  // keep the chains alive
+}
+
+}  // namespace
+
+extern "C" {
+
+// Runs the microbenchmark on the current device; *lane_ops_per_s receives
+// the best of `trials` launches (CUDA events), *ms the matching duration.
+// mix != 0: IADD3 + IMAD interleaved (ALU + FMA pipes, issue-bound);
+// mix == 0: IADD3 only (ALU pipe alone).
+int hrb_int_peak(int mix, int trials, double* lane_ops_per_s, float* ms) {
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 1;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    uint32_t* sink = nullptr;
+    if (cudaMalloc(&sink, 64) != cudaSuccess) return 1;
+    constexpr int REPS = 4096;
+    const int blocks = sms * 8, threads = 256;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    auto kern = mix ? int_peak_kernel<REPS, true> : int_peak_kernel<REPS, false>;
+    kern<<<blocks, threads>>>(1u, sink);  // warm-up
+    double best = 0;
+    float best_ms = 0;
+    for (int t = 0; t < (trials > 0 ? trials : 1); t++) {
+        cudaEventRecord(e0);
+        kern<<<blocks, threads>>>(2u + t, sink);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float m = 0;
+        cudaEventElapsedTime(&m, e0, e1);
+        const double ops = (double)blocks * threads * REPS * 8.0 * (mix ? 2.0 : 1.0);
+        const double v = ops / (m * 1e-3);
+        if (v > best) {
+            best = v;
+            best_ms = m;
+        }
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(sink);
+    if (cudaGetLastError() != cudaSuccess) return 1;
+    *lane_ops_per_s = best;
+    if (ms) *ms = best_ms;
+    return 0;
+}
+
+}  // extern "C"

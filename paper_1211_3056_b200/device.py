@@ -179,6 +179,74 @@ def run_host(batch: SliceBatch, algo_code: int, mode_code: int, split: int, cand
     return counts, fail[:nf], cm[:nc], cd[:nc], cdom[:nc], ms.value
 
 
+class HostRunner:
+    """hrb_run_slice_host with page-locked host buffers allocated once: the
+    slice inputs are copied into pinned memory at construction, outputs land
+    in pinned arrays.  Each run() is one C-ABI call (H2D of the slice, all
+    kernels, D2H of counts + failing ids + candidates, synchronised)."""
+
+    INPUTS = ("coef", "G", "s2abs", "n_dom", "dom_n", "last_n", "dom_base", "m0")
+
+    def __init__(self, batch: SliceBatch, algo_code: int, mode_code: int, split: int, cand_cap: int = 1 << 16):
+        torch = nat.require_cuda()
+        self.lib = nat.load()
+        self.batch, self.algo, self.mode, self.split = batch, algo_code, mode_code, split
+
+        def pinned(shape, dtype):
+            n = int(np.prod(shape)) * np.dtype(dtype).itemsize
+            t = torch.empty(max(n, 8), dtype=torch.uint8).pin_memory()
+            self._keep.append(t)
+            return t.numpy()[:n].view(dtype).reshape(shape)
+
+        self._keep = []
+        self.inputs = {}
+        for name in self.INPUTS:
+            src = np.ascontiguousarray(getattr(batch, name))
+            dst = pinned(src.shape, src.dtype)
+            dst[...] = src
+            self.inputs[name] = dst
+        p = {k: v.ctypes.data for k, v in self.inputs.items()}
+        self.desc = nat.HrbSlice(n_super=batch.n_super, n_total=batch.n_total, max_dom_n=batch.max_dom_n,
+                                 coef_limbs=batch.coef_limbs, frac_bits=batch.frac_bits, word_bits=batch.word_bits,
+                                 delta=batch.delta, coef=p["coef"], G=p["G"], s2abs=p["s2abs"], n_dom=p["n_dom"],
+                                 dom_n=p["dom_n"], last_n=p["last_n"], dom_base=p["dom_base"], m0=p["m0"])
+        self.counts = pinned((4,), np.uint64)
+        self.fail = pinned((max(batch.n_total, 1),), np.uint64)
+        self._alloc_cands(cand_cap)
+        self.device_ms = C.c_float(0)
+
+    def _alloc_cands(self, cap: int) -> None:
+        import torch
+
+        self.cand_cap = cap
+        bufs = [torch.empty(cap * 8, dtype=torch.uint8).pin_memory() for _ in range(3)]
+        self._cand_keep = bufs
+        self.cm, self.cd, self.cdom = (b.numpy().view(np.uint64) for b in bufs)
+
+    def input_bytes(self) -> int:
+        return sum(v.nbytes for v in self.inputs.values())
+
+    def run(self):
+        """One end-to-end call; returns (counts, fail_ids, cand_index,
+        cand_dist, cand_dom) as views of the pinned buffers."""
+        while True:
+            rc = self.lib.hrb_run_slice_host(C.byref(self.desc), self.algo, self.mode, self.split,
+                                             self.counts.ctypes.data, self.fail.ctypes.data, self.fail.size,
+                                             self.cm.ctypes.data, self.cd.ctypes.data, self.cdom.ctypes.data,
+                                             self.cand_cap, C.byref(self.device_ms))
+            if rc == nat.HRB_ERR_CAPACITY and int(self.counts[2]) > self.cand_cap:
+                self._alloc_cands(int(self.counts[2]))
+                continue
+            nat.check("hrb_run_slice_host", rc)
+            break
+        nf, nc = int(self.counts[0]), int(self.counts[2])
+        return self.counts, self.fail[:nf], self.cm[:nc], self.cd[:nc], self.cdom[:nc]
+
+    def output_bytes(self) -> int:
+        """Bytes the last run() copied device -> host."""
+        return 32 + 8 * int(self.counts[0]) + 24 * min(int(self.counts[2]), self.cand_cap)
+
+
 def domain_coefficients(ds: DeviceSlice) -> np.ndarray:
     """hrb_domain_coefficients -> uint32 [3, CL, n_total] (two's complement)."""
     torch = ds.torch

@@ -167,7 +167,12 @@ def build_super_domains(fn: str, binade: int, fmt: FpFormat, pg: PolyGenConfig, 
     mpmath host work, not the GPU, bounds large slices."""
     if count is None:
         count = (1 << (fmt.precision - 1)) - start
-    blocks = plan_blocks(fn, binade, fmt, pg, start, count, id0)
+    return supers_of_blocks(plan_blocks(fn, binade, fmt, pg, start, count, id0), workers)
+
+
+def supers_of_blocks(blocks: Sequence[_Block], workers: int = 1) -> list[SuperDomain]:
+    """Taylor model + hierarchical split of planned blocks, in block order."""
+    blocks = list(blocks)
     if workers > 1 and len(blocks) > 1:
         import multiprocessing as mp
 

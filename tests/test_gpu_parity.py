@@ -178,3 +178,20 @@ def test_per_phase_dropins():
     assert [[s.parent.domain.domain_id, s.sub_index, s.start, s.count] for s in subs] == [r[:4] for r in c["phase2"]]
     cands = phase3_exhaustive(subs, cfg)
     assert [[hex(x.argument), x.distance.raw, x.domain_id] for x in cands] == c["phase3"]
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_logical_shards_equal_reference(world):
+    """G logical shards on one device (the multi-GPU partition and merge)
+    reproduce the reference's candidates and records of the whole slice."""
+    from paper_1211_3056_b200.shard import run_logical_shards
+
+    c = case("p53_exp_2p20_e16_N12")
+    cfg = config_of(c)
+    lo, cnt = c["slice"]
+    merged, per_rank = run_logical_shards(c["fn"], c["binade"], lo, cnt, cfg, world)
+    cand = [[hex((int(h) << 64) | int(l)), int(d), int(i)] for h, l, d, i in merged.cand.tolist()]
+    assert cand == c["phase3"]
+    assert essence(merged.record_objects()) == c["records"]
+    assert int(merged.counters[0]) == len(c["phase1_fail"])
+    assert int(per_rank[:, 5].sum()) == cnt
