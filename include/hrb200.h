@@ -58,6 +58,20 @@ int hrb_search_batch(int algo, int mode, int word_bits, int64_t n, const uint64_
                      void* stream);
 
 /*
+ * hrb_search_batch plus the branch-decision stream of every problem: the
+ * `trace` list the reference cores append to (lowerbound.py:109-110,
+ * 126-127, 189-190, 246-259, 299-304), which its warp simulator consumes
+ * (divergence.py:243-248).  Decision k of problem i is bit (k mod 64) of
+ * trace_words[i * words_per_problem + k / 64]; trace_len[i] is the full
+ * decision count (decisions beyond 64 * words_per_problem are counted, not
+ * stored, so a caller can size a second call exactly).
+ */
+int hrb_search_trace(int algo, int mode, int word_bits, int64_t n, const uint64_t* a, const uint64_t* b,
+                     const uint64_t* eps, const uint64_t* count, uint8_t* ok, uint64_t* d, uint64_t* iterations,
+                     uint64_t* points_lo, uint8_t* points_hi, uint64_t* trace_words, int64_t words_per_problem,
+                     uint32_t* trace_len, void* stream);
+
+/*
  * A slice: S consecutive super-domains of one output-exponent piece run,
  * packed by the host after taylor_approx + hierarchical_split
  * (polygen.py:113-131, 193-252).  All arrays are device pointers, SoA.

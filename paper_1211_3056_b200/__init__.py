@@ -10,6 +10,19 @@ paper's hybrid CPU-GPU split.
 """
 
 from .arith import DivisionMode, MPInt, MPOverflowError, UFrac, frac_div
+from .divergence import (
+    BRANCH_WEIGHTS,
+    BranchWeights,
+    DivergenceReport,
+    WarpStats,
+    WarpTrace,
+    branch_serialization_estimate,
+    linear_problem_batch,
+    mdm,
+    measure_warps,
+    nmdm,
+    simulate_warps,
+)
 from .enclosure import UndecidedError, decide_hr, derivative_bound, enclose, value_exponent
 from .fpformat import (
     BinadeDomains,
@@ -101,6 +114,8 @@ def domain_coefficient_sets(r_polys, cfg: PolyGenConfig) -> list[tuple]:
 
 
 __all__ = [
+    "BRANCH_WEIGHTS", "BranchWeights", "DivergenceReport", "WarpStats", "WarpTrace", "branch_serialization_estimate",
+    "linear_problem_batch", "mdm", "measure_warps", "nmdm", "simulate_warps",
     "Algorithm", "BinadeDomains", "BinomialPoly", "DivisionMode", "Domain", "DomainTask", "ErrorBudget",
     "FpFormat", "HrCaseRecord", "MPInt", "MPOverflowError", "PhaseConfig", "PhaseRow", "PhaseStats",
     "PipelineConfig", "PolyGenConfig", "SEARCHES", "SearchOutcome", "SearchProblem", "SliceBatch",

@@ -918,6 +918,39 @@ __global__ void __launch_bounds__(256) search_batch_kernel(int algo, int mode, i
     }
 }
 
+// Same searches with the branch-decision stream of every problem recorded
+// (the reference cores' `trace` argument): bits LSB-first in
+// trace[i * wpp ...], the full decision count in trace_len[i] (decisions
+// past wpp * 64 are counted but not stored).
+template <int W>
+__global__ void __launch_bounds__(256) search_trace_kernel(int algo, int mode, int64_t n, const uint64_t* a,
+                                                           const uint64_t* b, const uint64_t* eps,
+                                                           const uint64_t* count, uint8_t* ok, uint64_t* d,
+                                                           uint64_t* it, uint64_t* pl, uint8_t* ph, uint64_t* trace,
+                                                           int64_t wpp, uint32_t* trace_len) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        hrb::BitTrace tr;
+        tr.words = trace + i * wpp;
+        tr.cap_bits = (uint32_t)(wpp * 64 < 0xFFFFFFFFll ? wpp * 64 : 0xFFFFFFFFll);
+        tr.len = 0;
+        hrb::Outcome o;
+        if (algo >= hrb::ALGO_REGULAR) {
+            const bool unr = algo == hrb::ALGO_REGULAR_UNROLLED;
+            o = hrb::regular_search<W, hrb::BitTrace>(a[i], b[i], eps[i], count[i], &tr, unr);
+            if (unr) o.it = (o.it + 1) >> 1;
+        } else {
+            o = hrb::lefevre_search<W, hrb::BitTrace>(a[i], b[i], eps[i], count[i], mode, &tr,
+                                                      algo == hrb::ALGO_LEFEVRE_SWAP);
+        }
+        ok[i] = o.ok;
+        d[i] = o.d;
+        if (it) it[i] = o.it;
+        pl[i] = o.pts_lo;
+        ph[i] = (uint8_t)o.pts_hi;
+        trace_len[i] = tr.len;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // workspace (per device, grows; guarded by a mutex)
 // ---------------------------------------------------------------------------
@@ -1146,6 +1179,29 @@ int hrb_search_batch(int algo, int mode, int word_bits, int64_t n, const uint64_
     else if (reg) SB(32, true);
     else SB(32, false);
 #undef SB
+    CK(cudaGetLastError());
+    return HRB_OK;
+}
+
+int hrb_search_trace(int algo, int mode, int word_bits, int64_t n, const uint64_t* a, const uint64_t* b,
+                     const uint64_t* eps, const uint64_t* count, uint8_t* ok, uint64_t* d, uint64_t* iterations,
+                     uint64_t* points_lo, uint8_t* points_hi, uint64_t* trace_words, int64_t words_per_problem,
+                     uint32_t* trace_len, void* stream) {
+    int rc = check_algo(algo, mode);
+    if (rc) return rc;
+    if (word_bits != 32 && word_bits != 64) return set_err(HRB_ERR_CONFIG, "word_bits must be 32 or 64");
+    if (n < 0 || words_per_problem < 0) return set_err(HRB_ERR_CONFIG, "negative size");
+    if (n == 0) return HRB_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t blocks = (n + 255) / 256;
+    const int cap = sm_count() * 16;
+    const int grid = (int)(blocks < cap ? blocks : cap);
+    if (word_bits == 64)
+        search_trace_kernel<64><<<grid, 256, 0, st>>>(algo, mode, n, a, b, eps, count, ok, d, iterations, points_lo,
+                                                      points_hi, trace_words, words_per_problem, trace_len);
+    else
+        search_trace_kernel<32><<<grid, 256, 0, st>>>(algo, mode, n, a, b, eps, count, ok, d, iterations, points_lo,
+                                                      points_hi, trace_words, words_per_problem, trace_len);
     CK(cudaGetLastError());
     return HRB_OK;
 }

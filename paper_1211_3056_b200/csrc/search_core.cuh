@@ -44,6 +44,26 @@ __device__ __forceinline__ Outcome mk_out(bool ok, uint64_t d, uint64_t it, uint
     return o;
 }
 
+// Branch-decision recorders: the device form of the reference cores' optional
+// `trace` list (lowerbound.py:88-308; consumed by divergence.py:243-248).
+struct NoTrace {
+    __device__ __forceinline__ void rec(bool) {}
+};
+
+struct BitTrace {  // decisions as bits, LSB first; len counts every decision
+    uint64_t* words;
+    uint32_t cap_bits;
+    uint32_t len;
+    __device__ __forceinline__ void rec(bool b) {
+        if (len < cap_bits) {
+            const uint64_t m = 1ull << (len & 63);
+            if (b) words[len >> 6] |= m;
+            else words[len >> 6] &= ~m;
+        }
+        len++;
+    }
+};
+
 // ~1/x to ~2^-44 relative: MUFU.RCP64H seed + one Newton step.
 __device__ __forceinline__ double recip_est(uint64_t x) {
     double xd = __ull2double_rn(x);
@@ -100,9 +120,9 @@ struct RegState {
 
 // Start a search.  Returns true if the search finished during setup (early
 // exits and the first half-step against one = 2^W) with *out filled.
-template <int W>
+template <int W, class Tr = NoTrace>
 __device__ __forceinline__ bool reg_begin(uint64_t a, uint64_t b, uint64_t eps, uint64_t N, RegState& st,
-                                          Outcome* out) {
+                                          Outcome* out, Tr* tr = nullptr, bool unrolled = false) {
     uint64_t d = b;
     if (d < eps) {
         *out = mk_out(false, d, 0, 1, 0);
@@ -117,6 +137,7 @@ __device__ __forceinline__ bool reg_begin(uint64_t a, uint64_t b, uint64_t eps, 
         return true;
     }
     uint64_t k, rem;
+    if (tr && !unrolled) tr->rec(true);  // iteration 1 is the then-body (p = a < q = one)
     if (W == 64) {
         if (a == 1) {
             // k = 2^64, q -> 0: d = b mod 1 = 0, points max(1 + 2^64, N) = 2^64 + 1
@@ -160,8 +181,8 @@ __device__ __forceinline__ bool reg_begin(uint64_t a, uint64_t b, uint64_t eps, 
 }
 
 // One half-step.  Returns true when the search finished (*out filled).
-template <int W>
-__device__ __forceinline__ bool reg_step(RegState& st, Outcome* out) {
+template <int W, class Tr = NoTrace>
+__device__ __forceinline__ bool reg_step(RegState& st, Outcome* out, Tr* tr = nullptr, bool unrolled = false) {
     const uint64_t S = st.S;
     double sinv = recip_est(S);
     uint64_t Lp;
@@ -169,6 +190,12 @@ __device__ __forceinline__ bool reg_step(RegState& st, Outcome* out) {
     uint64_t cLp = st.cL + k * st.cS;  // exact unless exhausted with S == 1 (see below)
     uint64_t d = st.d;
     uint64_t off = st.then_next ? 0 : Lp;
+    if (tr) {
+        // _regular_core: one decision per iteration (p < q);
+        // _regular_unrolled_core: the d >= p guard of each second half
+        if (!unrolled) tr->rec(st.then_next);
+        else if (!st.then_next) tr->rec(d >= Lp);
+    }
     if (d >= off) d = mod_est(d - off, S, sinv);
     st.it++;
     if (Lp == 0) {
@@ -201,12 +228,13 @@ __device__ __forceinline__ bool reg_step(RegState& st, Outcome* out) {
     return false;
 }
 
-template <int W>
-__device__ Outcome regular_search(uint64_t a, uint64_t b, uint64_t eps, uint64_t N) {
+template <int W, class Tr = NoTrace>
+__device__ Outcome regular_search(uint64_t a, uint64_t b, uint64_t eps, uint64_t N, Tr* tr = nullptr,
+                                  bool unrolled = false) {
     RegState st;
     Outcome o;
-    if (reg_begin<W>(a, b, eps, N, st, &o)) return o;
-    while (!reg_step<W>(st, &o)) {
+    if (reg_begin<W, Tr>(a, b, eps, N, st, &o, tr, unrolled)) return o;
+    while (!reg_step<W, Tr>(st, &o, tr, unrolled)) {
     }
     return o;
 }
@@ -255,13 +283,18 @@ __device__ __forceinline__ bool lef_begin(uint64_t a, uint64_t b, uint64_t eps, 
     return false;
 }
 
-template <int W>
-__device__ __forceinline__ bool lef_step(LefState& st, int mode, Outcome* out) {
+// trace polarity: _lefevre_swap_core records `swapped` (d >= p of the plain
+// walk), _lefevre_core records its complement (d < p); batched extras are
+// swapped-state decisions (lowerbound.py:109-148, 187-214)
+template <int W, class Tr = NoTrace>
+__device__ __forceinline__ bool lef_step(LefState& st, int mode, Outcome* out, Tr* tr = nullptr,
+                                         bool swap_polarity = false) {
     bool batched = st.in_batch && st.d >= st.q && st.q < st.p;
     if (batched) {
         if (mode == 1 && !st.extra) {
             st.it++;
             st.extra = true;
+            if (tr) tr->rec(swap_polarity);
         }
     } else {
         st.in_batch = false;
@@ -276,6 +309,7 @@ __device__ __forceinline__ bool lef_step(LefState& st, int mode, Outcome* out) {
             st.swapped = nxt;
         }
         st.it++;
+        if (tr) tr->rec(swap_polarity ? st.swapped : !st.swapped);
     }
     if (st.swapped) {
         st.d -= st.q;
@@ -320,12 +354,13 @@ __device__ __forceinline__ bool lef_step(LefState& st, int mode, Outcome* out) {
     return false;
 }
 
-template <int W>
-__device__ Outcome lefevre_search(uint64_t a, uint64_t b, uint64_t eps, uint64_t N, int mode) {
+template <int W, class Tr = NoTrace>
+__device__ Outcome lefevre_search(uint64_t a, uint64_t b, uint64_t eps, uint64_t N, int mode, Tr* tr = nullptr,
+                                  bool swap_polarity = false) {
     LefState st;
     Outcome o;
     if (lef_begin<W>(a, b, eps, N, st, &o)) return o;
-    while (!lef_step<W>(st, mode, &o)) {
+    while (!lef_step<W, Tr>(st, mode, &o, tr, swap_polarity)) {
     }
     return o;
 }

@@ -278,3 +278,36 @@ def search_batch_arrays(algo_code: int, mode_code: int, word_bits: int, a, b, ep
                                                        ph.data_ptr(), nat.stream_ptr()))
     torch.cuda.synchronize()
     return (ok[:n].cpu().numpy(), _u64(d[:n]), _u64(it[:n]), _u64(pl[:n]), ph[:n].cpu().numpy())
+
+
+def search_trace_arrays(algo_code: int, mode_code: int, word_bits: int, a, b, eps, count, device=None):
+    """hrb_search_trace over host arrays: the outcomes of search_batch_arrays
+    plus every problem's branch-decision list (the reference cores' `trace`).
+    Two passes: the first counts decisions, the second stores them."""
+    torch = nat.require_cuda()
+    lib = nat.load()
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    n = len(a)
+    ins = [torch.from_numpy(np.ascontiguousarray(np.asarray(x, dtype=np.uint64)).view(np.int64)).to(dev)
+           for x in (a, b, eps, count)]
+    m = max(n, 1)
+    ok = torch.empty(m, dtype=torch.uint8, device=dev)
+    d, it, pl = (torch.empty(m, dtype=torch.int64, device=dev) for _ in range(3))
+    ph = torch.empty(m, dtype=torch.uint8, device=dev)
+    tlen = torch.zeros(m, dtype=torch.int32, device=dev)
+    wpp = 1
+    while True:
+        words = torch.zeros(m * wpp, dtype=torch.int64, device=dev)
+        nat.check("hrb_search_trace", lib.hrb_search_trace(algo_code, mode_code, word_bits, n,
+                                                           *(x.data_ptr() for x in ins), ok.data_ptr(), d.data_ptr(),
+                                                           it.data_ptr(), pl.data_ptr(), ph.data_ptr(),
+                                                           words.data_ptr(), wpp, tlen.data_ptr(), nat.stream_ptr()))
+        torch.cuda.synchronize()
+        lens = tlen[:n].cpu().numpy().view(np.uint32).astype(np.int64)
+        need = int((lens.max() + 63) // 64) if n else 1
+        if need <= wpp:
+            break
+        wpp = need
+    bits = np.unpackbits(words.cpu().numpy().view(np.uint8).reshape(m, wpp * 8), axis=1, bitorder="little")
+    traces = [bits[i, : lens[i]].astype(bool).tolist() for i in range(n)]
+    return (ok[:n].cpu().numpy(), _u64(d[:n]), _u64(it[:n]), _u64(pl[:n]), ph[:n].cpu().numpy(), traces)

@@ -8,8 +8,8 @@ points_placed).  `search_many` is the batched form the pipeline uses; the
 per-problem callables exist for API completeness (one launch per call).
 
 The optional `trace` list of the reference (branch decisions, consumed by
-its warp *simulator*) has no device analogue: divergence is measured on the
-real hardware instead (per-lane iteration counts, ncu branch efficiency).
+its warp simulator) is served by hrb_search_trace, which records the same
+decision stream on the device.
 """
 
 from __future__ import annotations
@@ -97,9 +97,16 @@ def search_many(problems: Sequence[SearchProblem], algo: Algorithm | str = Algor
 
 def _single(algo: Algorithm):
     def run(problem: SearchProblem, mode: DivisionMode = DivisionMode.HYBRID, trace: list | None = None):
-        if trace is not None:
-            raise ValueError("branch traces are a simulator feature; the device reports per-lane iterations")
-        return search_many([problem], algo, mode)[0]
+        if trace is None:
+            return search_many([problem], algo, mode)[0]
+        from .device import search_trace_arrays
+
+        p = problem
+        ok, d, it, pl, ph, paths = search_trace_arrays(ALGO_CODE[algo], MODE_CODE[mode], p.a.width, [p.a.raw],
+                                                       [p.b.raw], [p.eps.raw], [p.count])
+        trace.extend(paths[0])
+        return SearchOutcome(Verdict.SUCCESS if ok[0] else Verdict.FAILURE, UFrac(int(d[0]), p.a.width), int(it[0]),
+                             int(pl[0]) | (int(ph[0]) << 64))
 
     run.__name__ = f"{algo.value}_lb"
     return run
