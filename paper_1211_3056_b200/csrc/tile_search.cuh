@@ -29,11 +29,17 @@ __device__ __forceinline__ double rcp_refined(double xd) {
     return fma(r, e, r);
 }
 
-// one search in flight, role form (see search_core.cuh RegState)
+// One search in flight.  The reference's (p, q) pair lives in two fixed
+// registers A, B whose roles alternate: before each else-half A is the
+// divisor (S) and B the dividend (L); the else-half replaces B by B mod A,
+// the following then-half replaces A by A mod B.  A loop iteration is one
+// (else, then) pair, so the state returns to the same registers with no
+// role-swap moves.  cA, cB are the matching point counts; Af, Bf the values
+// rounded to float (used only for quotient estimates).
 struct Slot {
-    uint64_t S, L, d;
-    float Sf, Lf;  // S, L rounded to float: only ever used for quotient estimates
-    uint32_t cS, cL;
+    uint64_t A, B, d;
+    float Af, Bf;
+    uint32_t cA, cB;
 };
 
 // Quotient estimate from the FP32 reciprocal: with M = 1.5 * 2^23 the FFMA
@@ -66,46 +72,116 @@ __device__ __forceinline__ float rcp_approx(float x) {
 
 constexpr int32_t QMAX = 1 << 20;
 
-// One half-step; THEN selects the reference's `p < q` body (d %= p) versus
-// the `p >= q` body (d reduced past the new p).  Returns true when the
-// search ended (verdict d > eps); the state is advanced unconditionally, so
-// a finished slot keeps computing harmless garbage.  Invariant S <= 2^63
-// (S is a remainder of 2^W by a, or smaller).
+// r -= S if r >= S; returns 1 if it subtracted (predicated IADD3 pair)
+__device__ __forceinline__ uint32_t csub(uint64_t& r, uint64_t S) {
+    uint32_t c;
+    asm("{\n\t.reg .pred p;\n\t"
+        "setp.ge.u64 p, %0, %2;\n\t"
+        "@p sub.u64 %0, %0, %2;\n\t"
+        "selp.u32 %1, 1, 0, p;\n\t}"
+        : "+l"(r), "=r"(c)
+        : "l"(S));
+    return c;
+}
+
+// One half-step, fast path: Lp = L mod S with its quotient k, and the
+// reduced d, from one FP32 reciprocal of S.  THEN selects the reference's
+// `p < q` body (d %= p) versus the `p >= q` body (d reduced past the new p;
+// when d < Lp, d < S already and the mod is the identity).  `big` flags a
+// quotient >= 2^20, where the estimate is not trusted (hs_exact redoes the
+// step).  Invariants on an active slot: S < L, d < L, S <= 2^63.
 template <bool THEN>
-__device__ __forceinline__ bool half_step(Slot& s, uint32_t N) {
-    const uint64_t S = s.S, L = s.L;
-    const float rcp = rcp_approx(s.Sf);
-    const int32_t ke = qest(s.Lf, rcp);
-    uint64_t Lp;
-    const uint32_t k = qfix(L, S, ke, Lp);
-    uint64_t cLp = (uint64_t)k * s.cS + s.cL;
-    // d reduction: then-body d mod S; else-body (d >= Lp ? d - Lp : d) mod S
-    // (when d < Lp, d < S already and the mod is the identity)
-    uint64_t x = (!THEN && s.d >= Lp) ? s.d - Lp : s.d;
-    const int32_t ke2 = qest(__ull2float_rn(x), rcp);
-    uint64_t dn;
-    qfix(x, S, ke2, dn);
-    if (ke >= QMAX || ke2 >= QMAX) {  // rare: a quotient >= 2^20 (exact path)
-        const uint64_t kk = S ? L / S : 0;
-        Lp = L - kk * S;
-        cLp = kk * (uint64_t)s.cS + s.cL;  // true value <= 2^64; == 2^64 only if Lp == 0 and S == 1
-        x = (!THEN && s.d >= Lp) ? s.d - Lp : s.d;
-        dn = S ? x % S : x;
-    }
-    s.d = dn;
-    const bool done = Lp == 0 || cLp >= (uint64_t)(N - s.cS);
-    s.L = S;
-    s.Lf = s.Sf;
-    s.S = Lp;
-    s.Sf = __ull2float_rn(Lp);
-    s.cL = s.cS;
-    s.cS = (uint32_t)cLp;
+__device__ __forceinline__ void hs_fast(uint64_t L, uint64_t S, float Lf, float Sf, uint64_t d, uint64_t& Lp,
+                                        uint64_t& dn, uint32_t& k, bool& big) {
+    const float rcp = rcp_approx(Sf);
+    const int32_t ke = qest(Lf, rcp);  // >= 0 because L > S
+    big = ke >= QMAX;
+    uint64_t r = L - (uint64_t)(uint32_t)ke * S;
+    k = (uint32_t)ke + csub(r, S);
+    uint64_t x = d;
+    if (!THEN) csub(x, r);
+    // quotient of x by S is >= 0, so the estimate is >= -1 (clamped to 0,
+    // where x < S already holds)
+    const uint32_t ke2 = (uint32_t)max(qest(__ull2float_rn(x), rcp), 0);
+    uint64_t y = x - (uint64_t)ke2 * S;
+    csub(y, S);
+    Lp = r;
+    dn = y;
+}
+
+// The same half-step with hardware 64-bit division (rare: quotient >= 2^20).
+// k saturates at 2^32 - 1: any quotient that large ends the search (cS >= 1
+// makes cLp >= 2^32 - 1 >= N - cS), exactly as the reference's u + v >= N.
+// Out of line and by value, so the hot loop keeps its registers.
+struct ExactStep {
+    uint64_t Lp, dn;
+    uint32_t k;
+};
+
+__device__ __noinline__ ExactStep hs_exact(uint64_t L, uint64_t S, uint64_t d, bool then_body) {
+    ExactStep e;
+    const uint64_t kk = L / S;
+    e.Lp = L - kk * S;
+    const uint64_t x = (!then_body && d >= e.Lp) ? d - e.Lp : d;
+    e.dn = x % S;
+    e.k = kk > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)kk;
+    return e;
+}
+
+// Commit a half-step in place (L <- Lp, cL <- k cS + cL, d <- dn) and report
+// whether the search ended: expansion exhausted (Lp == 0) or the count
+// reaches N.  A finished slot keeps computing harmless garbage.
+__device__ __forceinline__ bool hs_commit(uint64_t& L, float& Lf, uint32_t& cL, uint32_t cS, uint64_t& d, uint32_t N,
+                                          uint64_t Lp, uint64_t dn, uint32_t k) {
+    const uint64_t cLp = (uint64_t)k * cS + cL;
+    const bool done = Lp == 0 || cLp >= (uint64_t)(N - cS);
+    L = Lp;
+    Lf = __ull2float_rn(Lp);
+    cL = (uint32_t)cLp;
+    d = dn;
     return done;
+}
+
+// Both slots of a lane advance one half-step: the else-half divides B by A,
+// the then-half A by B.  Must be called by all 32 lanes of the warp
+// (warp-uniform control flow): the rare exact path is entered by the whole
+// warp through one vote, so the hot path carries no divergent branch.
+template <bool THEN>
+__device__ __forceinline__ void pair_step(Slot& s0, Slot& s1, uint32_t n0, uint32_t n1, bool act0, bool act1,
+                                          bool& f0, bool& f1) {
+    uint64_t& L0 = THEN ? s0.A : s0.B;
+    uint64_t& L1 = THEN ? s1.A : s1.B;
+    const uint64_t S0 = THEN ? s0.B : s0.A, S1 = THEN ? s1.B : s1.A;
+    float& Lf0 = THEN ? s0.Af : s0.Bf;
+    float& Lf1 = THEN ? s1.Af : s1.Bf;
+    const float Sf0 = THEN ? s0.Bf : s0.Af, Sf1 = THEN ? s1.Bf : s1.Af;
+    uint32_t& cL0 = THEN ? s0.cA : s0.cB;
+    uint32_t& cL1 = THEN ? s1.cA : s1.cB;
+    const uint32_t cS0 = THEN ? s0.cB : s0.cA, cS1 = THEN ? s1.cB : s1.cA;
+    uint64_t Lp0, dn0, Lp1, dn1;
+    uint32_t k0, k1;
+    bool b0, b1;
+    hs_fast<THEN>(L0, S0, Lf0, Sf0, s0.d, Lp0, dn0, k0, b0);
+    hs_fast<THEN>(L1, S1, Lf1, Sf1, s1.d, Lp1, dn1, k1, b1);
+    b0 = b0 && act0;
+    b1 = b1 && act1;
+    if (__any_sync(0xffffffffu, b0 || b1)) {
+        if (b0) {
+            const ExactStep e = hs_exact(L0, S0, s0.d, THEN);
+            Lp0 = e.Lp, dn0 = e.dn, k0 = e.k;
+        }
+        if (b1) {
+            const ExactStep e = hs_exact(L1, S1, s1.d, THEN);
+            Lp1 = e.Lp, dn1 = e.dn, k1 = e.k;
+        }
+    }
+    f0 = hs_commit(L0, Lf0, cL0, cS0, s0.d, n0, Lp0, dn0, k0);
+    f1 = hs_commit(L1, Lf1, cL1, cS1, s1.d, n1, Lp1, dn1, k1);
 }
 
 // _regular_core up to and including the first (then-) half-step against
 // one = 2^W.  Returns true if the search ended there (*ok, *it set);
-// otherwise `s` holds the state before the first else-half.
+// otherwise `s` holds the state before the first else-half (A < B).
 template <int W>
 __device__ __forceinline__ bool reg_start(uint64_t a, uint64_t b, uint64_t eps, uint32_t N, Slot& s, bool* ok,
                                           uint32_t* it) {
@@ -160,13 +236,13 @@ __device__ __forceinline__ bool reg_start(uint64_t a, uint64_t b, uint64_t eps, 
         *it = 1;
         return true;
     }
-    s.S = rem;
-    s.L = a;
+    s.A = rem;  // divisor of the first else-half
+    s.B = a;
     s.d = d;
-    s.Sf = __ull2float_rn(rem);
-    s.Lf = __ull2float_rn(a);
-    s.cS = (uint32_t)k;
-    s.cL = 1;
+    s.Af = __ull2float_rn(rem);
+    s.Bf = __ull2float_rn(a);
+    s.cA = (uint32_t)k;
+    s.cB = 1;
     return false;
 }
 
@@ -176,10 +252,15 @@ __device__ __forceinline__ bool reg_start(uint64_t a, uint64_t b, uint64_t eps, 
 // Returns the lane's failure bits (bit k = item k failed) and adds the
 // items' iteration counts (halved and rounded up for the unrolled variant)
 // to *iters.
+//
+// Must be called by all 32 lanes of a warp: the item and step loops run to the
+// warp's maximum (items past a lane's own count build as invalid), which keeps
+// the vote in pair_step legal and the loop branches uniform.
 template <int W, int NU, class Src>
 __device__ __forceinline__ uint32_t lane_items(Src& src, unsigned long long* iters, bool halve, uint32_t n_items = NU) {
     uint32_t fails = 0, its = 0;
-    const int kend = n_items < (uint32_t)NU ? (int)n_items : NU;
+    const uint32_t mine = n_items < (uint32_t)NU ? n_items : (uint32_t)NU;
+    const int kend = (int)__reduce_max_sync(0xffffffffu, mine);
 #pragma unroll 1
     for (int k = 0; k < kend; k += 2) {
         Slot s0, s1;
@@ -211,9 +292,9 @@ __device__ __forceinline__ uint32_t lane_items(Src& src, unsigned long long* ite
             n1 = n0;
         }
         uint32_t h = 1;  // half-steps so far (both slots start after their first then-half)
-        while (act0 || act1) {
-            bool f0 = half_step<false>(s0, n0);
-            bool f1 = half_step<false>(s1, n1);
+        while (__any_sync(0xffffffffu, act0 || act1)) {
+            bool f0, f1;
+            pair_step<false>(s0, s1, n0, n1, act0, act1, f0, f1);
             h++;
             if (act0 && f0) {
                 its += halve ? (h + 1) >> 1 : h;
@@ -225,8 +306,7 @@ __device__ __forceinline__ uint32_t lane_items(Src& src, unsigned long long* ite
                 fails |= (s1.d > e1) ? 0u : 2u << k;
                 act1 = false;
             }
-            f0 = half_step<true>(s0, n0);
-            f1 = half_step<true>(s1, n1);
+            pair_step<true>(s0, s1, n0, n1, act0, act1, f0, f1);
             h++;
             if (act0 && f0) {
                 its += halve ? (h + 1) >> 1 : h;

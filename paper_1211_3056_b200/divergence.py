@@ -49,25 +49,16 @@ def _slope(fn: str, x: Fraction, value: Fraction, prec: int) -> Fraction:
     raise ValueError(f"unsupported function {fn!r}")
 
 
-def linear_problem_batch(fn: str, fmt, binade: int, domain_size: int, domain_count: int | None = None,
-                         word_bits: int = 64, eps: Fraction | None = None) -> list[SearchProblem]:
-    """One linearised problem per subdomain of `domain_size` consecutive
-    arguments of the binade: b = {2^(p-e) f(x0)}, a = {f'(x0) ulp 2^(p-e)},
-    eps = 2 eps_fmt, count = the subdomain size (divergence.py:32-93)."""
+def _linear_problems(args) -> list[SearchProblem]:
     from .enclosure import enclose, value_exponent
     from .fpformat import Domain
 
-    if domain_size < 1:
-        raise ValueError("domain_size must be >= 1")
+    fn, fmt, binade, domain_size, total, starts, word_bits, eps = args
     half = 1 << (fmt.precision - 1)
-    total = half if domain_count is None else domain_count * domain_size
-    if not 1 <= total <= half:
-        raise ValueError("batch does not fit in one binade")
-    eps = fmt.eps if eps is None else eps
     prec = word_bits + 32
     ulp = Fraction(1, 1 << (fmt.precision - 1 - binade))
     out = []
-    for start in range(0, total, domain_size):
+    for start in starts:
         x = Domain(half + start, binade + 1, 1, 0).x_at(0, fmt)
         scale = Fraction(2) ** (fmt.precision - value_exponent(fn, x))
         lo, hi = enclose(fn, x, prec)
@@ -76,6 +67,31 @@ def linear_problem_batch(fn: str, fmt, binade: int, domain_size: int, domain_cou
         out.append(SearchProblem(UFrac.from_fraction(a, word_bits), UFrac.from_fraction((mid * scale) % 1, word_bits),
                                  UFrac.from_fraction(2 * eps, word_bits), min(domain_size, total - start)))
     return out
+
+
+def linear_problem_batch(fn: str, fmt, binade: int, domain_size: int, domain_count: int | None = None,
+                         word_bits: int = 64, eps: Fraction | None = None, workers: int = 1) -> list[SearchProblem]:
+    """One linearised problem per subdomain of `domain_size` consecutive
+    arguments of the binade: b = {2^(p-e) f(x0)}, a = {f'(x0) ulp 2^(p-e)},
+    eps = 2 eps_fmt, count = the subdomain size (divergence.py:32-93).
+    `workers` > 1 spreads the (independent) enclosures over host processes."""
+    if domain_size < 1:
+        raise ValueError("domain_size must be >= 1")
+    half = 1 << (fmt.precision - 1)
+    total = half if domain_count is None else domain_count * domain_size
+    if not 1 <= total <= half:
+        raise ValueError("batch does not fit in one binade")
+    eps = fmt.eps if eps is None else eps
+    starts = list(range(0, total, domain_size))
+    if workers <= 1 or len(starts) < 2 * workers:
+        return _linear_problems((fn, fmt, binade, domain_size, total, starts, word_bits, eps))
+    import multiprocessing as mp
+
+    chunk = -(-len(starts) // (workers * 4))
+    jobs = [(fn, fmt, binade, domain_size, total, starts[k:k + chunk], word_bits, eps)
+            for k in range(0, len(starts), chunk)]
+    with mp.get_context("fork").Pool(workers) as pool:
+        return [p for part in pool.map(_linear_problems, jobs) for p in part]
 
 
 def problem_arrays(problems: Sequence[SearchProblem]):
