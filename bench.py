@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--log2-args", type=int, default=40, help="arguments per GPU (log2)")
     ap.add_argument("--eps-bits", type=int, default=32)
+    ap.add_argument("--fn", default="exp", choices=("exp", "log", "exp2"))
+    ap.add_argument("--start", type=lambda x: int(x, 0), default=0, help="first binade argument index of the range")
     ap.add_argument("--algo", default="regular", choices=("regular", "lefevre"))
     ap.add_argument("--log2-super", type=int, default=24)
     ap.add_argument("--log2-N", type=int, default=15)
@@ -71,7 +73,7 @@ def make_cfg(args):
     tau = 1 << (args.log2_super - args.log2_N)
     mu = 1 << ((args.log2_super - args.log2_N) // 2)
     pg = PolyGenConfig(tau=tau, N=N, mu=mu, nu=tau // mu, delta=2, limbs=8, frac_bits=96, guard=32)
-    return PipelineConfig("exp", FpFormat(53, args.eps_bits), pg, PhaseConfig(args.algo, phase2_split=8, N1=N))
+    return PipelineConfig(args.fn, FpFormat(53, args.eps_bits), pg, PhaseConfig(args.algo, phase2_split=8, N1=N))
 
 
 def prepare_rank(args, rank, world, workers):
@@ -81,7 +83,7 @@ def prepare_rank(args, rank, world, workers):
 
     cfg = make_cfg(args)
     t0 = time.perf_counter()
-    blocks = plan_blocks("exp", 0, cfg.fmt, cfg.polygen, 0, world << args.log2_args)
+    blocks = plan_blocks(args.fn, 0, cfg.fmt, cfg.polygen, args.start, world << args.log2_args)
     b0, b1 = partition_blocks([b.bcount for b in blocks], world)[rank]
     supers = supers_of_blocks(blocks[b0:b1], workers)
     batch = pack_slice(supers, cfg.fmt, cfg.polygen, cfg.word_bits, 0)
@@ -89,7 +91,8 @@ def prepare_rank(args, rank, world, workers):
 
 
 def workload_name(args):
-    return (f"exp p=53 [1,2) 2^{args.log2_args} args/GPU eps=2^-{args.eps_bits} N=2^{args.log2_N} "
+    start = f" from index {args.start:#x}" if args.start else ""
+    return (f"{args.fn} p=53 [1,2){start} 2^{args.log2_args} args/GPU eps=2^-{args.eps_bits} N=2^{args.log2_N} "
             f"super=2^{args.log2_super} delta=2 F=96 W=64 split=8 {args.algo}")
 
 
@@ -195,7 +198,7 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u64",
-            "data": "synthetic: exp binade [1,2) argument range (real Taylor blocks)",
+            "data": f"synthetic: {args.fn} binade [1,2) argument range (real Taylor blocks)",
             "config": {"workload": workload_name(args), "parallelism": "host threads (OpenMP)"},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": oracle.threads(), "kind": "port",
                              "sample": f"the full per-GPU workload, phases 1-3, {args.steps} timed runs"},
@@ -211,7 +214,7 @@ def int_peak():
     lib = C.CDLL(PEAK_LIB)
     lib.hrb_int_peak.argtypes = [C.c_int, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_float)]
     out = {}
-    for mix, key in ((1, "alu_fma"), (0, "alu_only")):
+    for mix, key in ((1, "iadd3_imad"), (0, "iadd3_lop3")):
         v, ms = C.c_double(0), C.c_float(0)
         if lib.hrb_int_peak(mix, 5, C.byref(v), C.byref(ms)) != 0:
             raise RuntimeError("hrb_int_peak failed")
@@ -338,25 +341,32 @@ def main():
     # ---- roofline of the dominant kernel (phase 1): INT-pipe bound
     peak = int_peak()
     calib = load_calibration()
+    sys.path.insert(0, os.path.join(ROOT, "scripts"))
+    from make_calibration import source_sha
+
     k1 = calib.get("phase1_reg_kernel", {})
     lane_per_step = k1.get("int_lane_instr_per_quotient_step")
     achieved = iters * lane_per_step / (p1_max / 1e3) if lane_per_step else None
+    p_int = max(peak.values())
     roofline = {"bound": "int", "kernel": "phase1_reg_kernel (+ ordered compaction)", "unit": "Tops/s",
-                "achieved": achieved / 1e12 if achieved else None, "peak": peak["alu_fma"] / 1e12,
-                "peak_basis": "measured: IADD3+IMAD dependency chains on all SMs (csrc/intpeak.cu), lane-ops/s",
-                "frac": achieved / peak["alu_fma"] if achieved else None,
-                "alu_only_peak": peak["alu_only"] / 1e12,
+                "achieved": achieved / 1e12 if achieved else None, "peak": p_int / 1e12,
+                "peak_basis": "measured on this GPU: integer dependency chains on all SMs (csrc/intpeak.cu), "
+                              "SASS integer instructions x 32 lanes / s; best of IADD3+IMAD and IADD3+LOP3 mixes",
+                "frac": achieved / p_int if achieved else None,
+                "peak_probes": {k: v / 1e12 for k, v in peak.items()},
                 "traffic": k1.get("dram_bytes_per_launch"),
                 "algorithmic_unit": "CF quotient step (SearchOutcome.iterations)",
                 "quotient_steps_per_launch": iters, "kernel_ms": p1_max,
                 "quotient_steps_per_s": iters / (p1_max / 1e3),
                 "int_lane_instr_per_quotient_step": lane_per_step,
                 "calibration": os.path.relpath(CALIBRATION, ROOT) if k1 else None,
+                "calibration_stale": (calib.get("source_sha") != source_sha()) if k1 else None,
+                "calibration_steps_match": (k1.get("quotient_steps") == iters) if k1 else None,
                 "phase_ms_incl_compaction": phase_ms}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u64",
-            "data": "synthetic: exp binade [1,2) argument ranges, Taylor blocks generated on the host (mpmath)",
+            "data": f"synthetic: {args.fn} binade [1,2) argument ranges, Taylor blocks generated on the host (mpmath)",
             "config": {"workload": workload_name(args),
                        "parallelism": f"shard{world} (contiguous super-domain blocks, no collective on the hot path; "
                                       f"NCCL gather of counters + candidates at the end)",

@@ -1,12 +1,13 @@
 // intpeak.cu -- measured INT-pipe peak of the device (roofline denominator).
 //
 // Not part of the C-ABI of include/hrb200.h: a measurement tool that bench.py
-// loads beside it.  Every thread runs 8 independent dependency chains of
-// 32-bit integer adds (IADD3, ALU pipe) and 8 of integer multiply-adds
-// (IMAD, FMA pipe), interleaved, so the SM sub-partition schedulers can
-// issue one integer warp-instruction per clock (the issue limit).  The
-// returned figure is lane-ops/s = warp-instructions * 32 / seconds, the same
-// unit the HR kernels' achieved INT throughput is quoted in.
+// loads beside it.  mix = 1: every chain step is one IADD3 (ALU pipe) plus
+// one IMAD (FMA pipe), so the sub-partition schedulers can issue one integer
+// warp-instruction per clock, the INT issue limit of the SM (ALU and FMA
+// pipes each accept one warp-instruction every 2 clocks per sub-partition).
+// mix = 0: IADD3 + LOP3, both on the ALU pipe alone.  The returned figure is
+// lane-ops/s = SASS integer instructions * 32 lanes / seconds, the unit the
+// HR kernels' achieved INT throughput is quoted in.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -14,26 +15,30 @@ namespace {
 
 template <int REPS, bool MIX>
 __global__ void __launch_bounds__(256) int_peak_kernel(uint32_t seed, uint32_t* sink) {
-    uint32_t a[8], m[8];
+    // 8 independent chains of two mutually dependent registers: every result
+    // feeds the next operation, so ptxas can neither fold nor fuse them
+    // (two SASS instructions per chain step, checked with cuobjdump / ncu)
+    uint32_t a[8], b[8];
 #pragma unroll
     for (int k = 0; k < 8; k++) {
         a[k] = seed + threadIdx.x * 7u + k;
-        m[k] = seed ^ (threadIdx.x + 13u * k);
+        b[k] = seed ^ (threadIdx.x + 13u * k);
     }
-    const uint32_t c = seed | 1u;
-#pragma unroll 8
+    const uint32_t c = seed | 3u;
+#pragma unroll 4
     for (int r = 0; r < REPS; r++) {
 #pragma unroll
         for (int k = 0; k < 8; k++) {
-            // IADD3 on the ALU pipe
-            asm volatile("add.u32 %0, %0, %1;" : "+r"(a[k]) : "r"(c));
-            // IMAD on the FMA pipe (mix == 0: ALU only)
-            if (MIX) asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(m[k]) : "r"(c), "r"(a[k]));
+            asm volatile("add.u32 %0, %0, %1;" : "+r"(a[k]) : "r"(b[k]));  // IADD3, ALU pipe
+            if (MIX)
+                asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(b[k]) : "r"(c), "r"(a[k]));  // IMAD, FMA pipe
+            else
+                asm volatile("xor.b32 %0, %0, %1;" : "+r"(b[k]) : "r"(a[k]));  // LOP3, ALU pipe
         }
     }
     uint32_t x = 0;
 #pragma unroll
-    for (int k = 0; k < 8; k++) x ^= a[k] ^ m[k];
+    for (int k = 0; k < 8; k++) x ^= a[k] ^ b[k];
     if (x == 0x9E3779B9u) sink[0] = x;  // keep the chains alive
 }
 
@@ -67,7 +72,7 @@ int hrb_int_peak(int mix, int trials, double* lane_ops_per_s, float* ms) {
         cudaEventSynchronize(e1);
         float m = 0;
         cudaEventElapsedTime(&m, e0, e1);
-        const double ops = (double)blocks * threads * REPS * 8.0 * (mix ? 2.0 : 1.0);
+        const double ops = (double)blocks * threads * REPS * 8.0 * 2.0;
         const double v = ops / (m * 1e-3);
         if (v > best) {
             best = v;
