@@ -186,17 +186,43 @@ def execute_batch(batch: SliceBatch, cfg: PipelineConfig, algo: str, fn: str | N
     records = []
     t4 = time.perf_counter()
     if confirm:
-        fn = fn or cfg.fn
-        guard = 2 * (fmt.precision + fmt.eps_bits) + 16
-        for c in cand:
-            dec = decide_hr(fn, bits_float(c.argument, fmt), fmt, start_prec=guard)
-            if dec.is_hr:
-                records.append(HrCaseRecord(c.argument, UFrac.from_fraction(dec.distance_lo), c.domain_id))
-        records.sort()
+        records = confirm_candidates(fn or cfg.fn, cand, fmt, cfg.phase.parallel_width)
     stats.rows.append(PhaseRow("confirm", len(cand), len(records), len(cand), (time.perf_counter() - t4) * 1e3))
     rows = list(zip((id0 + sub_local).tolist(), sub_j.tolist(), sub_start.tolist(), sub_cnt.tolist()))
     return SliceOutput(batch, [id0 + int(x) for x in res.fail_ids.tolist()], rows, cand, records, stats,
                        res.iterations)
+
+
+def _confirm_chunk(job) -> list:
+    fn, fmt, cands = job
+    guard = 2 * (fmt.precision + fmt.eps_bits) + 16
+    out = []
+    for c in cands:
+        dec = decide_hr(fn, bits_float(c.argument, fmt), fmt, start_prec=guard)
+        if dec.is_hr:
+            out.append(HrCaseRecord(c.argument, UFrac.from_fraction(dec.distance_lo), c.domain_id))
+    return out
+
+
+CONFIRM_CHUNK = 64
+
+
+def confirm_candidates(fn: str, cand: Sequence[HrCaseRecord], fmt: FpFormat, workers: int = 1) -> list:
+    """Rigorous confirmation of phase-3 candidates (pipeline.py:447-462):
+    decide_hr at rising precision per candidate, records sorted.  The
+    candidates are independent, so workers > 1 spreads them over host
+    processes (the result is order-independent: it is sorted)."""
+    cand = list(cand)
+    if workers > 1 and len(cand) > 2 * CONFIRM_CHUNK:
+        import multiprocessing as mp
+
+        jobs = [(fn, fmt, cand[k:k + CONFIRM_CHUNK]) for k in range(0, len(cand), CONFIRM_CHUNK)]
+        with mp.get_context("fork").Pool(workers) as pool:
+            records = [r for part in pool.map(_confirm_chunk, jobs) for r in part]
+    else:
+        records = _confirm_chunk((fn, fmt, cand))
+    records.sort()
+    return records
 
 
 def prepare_slice(fn: str, binade: int, start: int, count: int, cfg: PipelineConfig, workers: int | None = None,

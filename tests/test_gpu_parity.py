@@ -195,3 +195,70 @@ def test_logical_shards_equal_reference(world):
     assert essence(merged.record_objects()) == c["records"]
     assert int(merged.counters[0]) == len(c["phase1_fail"])
     assert int(per_rank[:, 5].sum()) == cnt
+
+
+def _big_slice(fn, start, log2_count, eps_bits, algo="regular", N=1 << 15, super_log2=24):
+    from paper_1211_3056_b200 import FpFormat, PhaseConfig, PipelineConfig, PolyGenConfig
+    from paper_1211_3056_b200.funnel import prepare_slice
+
+    tau = (1 << super_log2) // N
+    mu = 1 << ((tau.bit_length() - 1) // 2)
+    pg = PolyGenConfig(tau=tau, N=N, mu=mu, nu=tau // mu, delta=2, limbs=8, frac_bits=96, guard=32)
+    cfg = PipelineConfig(fn, FpFormat(53, eps_bits), pg, PhaseConfig(algo, phase2_split=8, N1=N))
+    import os
+
+    return prepare_slice(fn, 0, start, 1 << log2_count, cfg, workers=os.cpu_count() or 1), cfg
+
+
+@pytest.mark.parametrize("fn,start,log2_count,eps_bits,algo", [
+    ("exp", 0, 36, 24, "regular"),          # C5-shaped: loose eps, many candidates
+    ("exp", 1 << 44, 34, 32, "lefevre"),    # classic walk in the fused pipeline
+    ("log", 0x6A09E667F3BCD, 34, 28, "regular"),  # C4-shaped: log near sqrt(2)
+])
+def test_large_slice_fused_equals_oracle(fn, start, log2_count, eps_bits, algo):
+    """Full outputs of hrb_run_slice at 2^34-2^36 arguments (thousands of
+    super-domains) equal the CPU oracle's: failing ids, surviving
+    subdomains, candidates (argument, distance, domain)."""
+    from paper_1211_3056_b200.device import DeviceSlice, FusedRunner
+
+    batch, cfg = _big_slice(fn, start, log2_count, eps_bits, algo)
+    code = ALGO_CODE[algo]
+    fused = FusedRunner(DeviceSlice(batch), code, 1, 8, sub_cap=batch.n_total * 16, cand_cap=1 << 22)
+    fused.launch()
+    r = fused.result()
+    want1 = oracle.phase1(batch, algo, 1)
+    assert np.array_equal(r.fail_ids + np.uint64(batch.id0), want1)
+    rows = oracle.phase2(batch, algo, 1, 8, want1)
+    got_keys = (r.sub_keys >> np.uint64(8)) + np.uint64(batch.id0)
+    assert np.array_equal(got_keys, rows[0]) and np.array_equal(r.sub_keys & np.uint64(255), rows[1].astype(np.uint64))
+    m, dist, dom = oracle.phase3(batch, rows)
+    assert np.array_equal(r.cand_index, m) and np.array_equal(r.cand_dist, dist)
+    assert np.array_equal(r.cand_dom + np.uint64(batch.id0), dom)
+    assert len(m) > 0 or eps_bits >= 28
+
+
+def test_large_slice_logical_shards_and_rerun_are_identical():
+    """Determinism and shard invariance at 2^36: 4 logical shards merged in
+    rank order equal the single run, and a re-launch reproduces it."""
+    from paper_1211_3056_b200.device import DeviceSlice, FusedRunner
+    from paper_1211_3056_b200.shard import partition_blocks
+    from paper_1211_3056_b200.slices import slice_view
+
+    batch, cfg = _big_slice("exp", 0, 36, 20)
+    whole = FusedRunner(DeviceSlice(batch), 2, 1, 8, sub_cap=batch.n_total * 16, cand_cap=1 << 22)
+    whole.launch()
+    a = whole.result()
+    whole.launch()
+    b = whole.result()
+    assert np.array_equal(a.cand_index, b.cand_index) and np.array_equal(a.fail_ids, b.fail_ids)
+    parts = partition_blocks([s.count for s in batch.supers], 4)
+    fails, cands = [], []
+    for t0, t1 in parts:
+        sub = slice_view(batch, t0, t1)
+        fr = FusedRunner(DeviceSlice(sub), 2, 1, 8, sub_cap=sub.n_total * 16, cand_cap=1 << 22)
+        fr.launch()
+        rr = fr.result()
+        fails.append(rr.fail_ids + np.uint64(sub.id0 - batch.id0))
+        cands.append(rr.cand_index)
+    assert np.array_equal(np.concatenate(fails), a.fail_ids)
+    assert np.array_equal(np.concatenate(cands), a.cand_index)

@@ -34,3 +34,21 @@ def test_parallel_generation_is_identical():
     a = build_super_domains(c["fn"], c["binade"], cfg.fmt, cfg.polygen, lo, cnt, workers=1)
     b = build_super_domains(c["fn"], c["binade"], cfg.fmt, cfg.polygen, lo, cnt, workers=4)
     assert a == b
+
+
+@pytest.mark.parametrize("workers", [1, 3])
+def test_confirmation_matches_reference_records(workers, monkeypatch):
+    """Host confirmation (decide_hr per phase-3 candidate, pipeline.py:447-462),
+    serial and spread over processes, gives the reference's records."""
+    from golden_io import essence
+    from paper_1211_3056_b200 import funnel
+    from paper_1211_3056_b200.arith import UFrac
+    from paper_1211_3056_b200.fpformat import HrCaseRecord
+
+    monkeypatch.setattr(funnel, "CONFIRM_CHUNK", 4)
+    for name in ("p53_exp_2p20_e16_N12", "p53_log_sqrt2_e16", "p13_exp_b0"):
+        c = case(name)
+        cfg = config_of(c)
+        cand = [HrCaseRecord(int(h, 16), UFrac(d, 64), i) for h, d, i in c["phase3"]]
+        recs = funnel.confirm_candidates(c["fn"], cand, cfg.fmt, workers)
+        assert essence(recs) == c["records"], name
