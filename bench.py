@@ -353,6 +353,9 @@ def main():
                 "peak_basis": "measured on this GPU: integer dependency chains on all SMs (csrc/intpeak.cu), "
                               "SASS integer instructions x 32 lanes / s; best of IADD3+IMAD and IADD3+LOP3 mixes",
                 "frac": achieved / p_int if achieved else None,
+                "issue_limit": 148 * 128 * (clocks.get("sm_mhz") or 1965.0) * 1e6 / 1e12,
+                "frac_of_issue_limit": achieved / (148 * 128 * (clocks.get("sm_mhz") or 1965.0) * 1e6)
+                if achieved else None,
                 "peak_probes": {k: v / 1e12 for k, v in peak.items()},
                 "traffic": k1.get("dram_bytes_per_launch"),
                 "algorithmic_unit": "CF quotient step (SearchOutcome.iterations)",

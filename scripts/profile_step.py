@@ -15,10 +15,13 @@ def main():
     ap.add_argument("--log2-args", type=int, default=40)
     ap.add_argument("--eps-bits", type=int, default=32)
     ap.add_argument("--algo", default="regular")
+    ap.add_argument("--fn", default="exp")
+    ap.add_argument("--start", type=lambda x: int(x, 0), default=0)
     ap.add_argument("--launches", type=int, default=1)
     ap.add_argument("--no-peak", action="store_true")
     a = ap.parse_args()
-    ns = argparse.Namespace(log2_args=a.log2_args, eps_bits=a.eps_bits, algo=a.algo, log2_super=24, log2_N=15)
+    ns = argparse.Namespace(log2_args=a.log2_args, eps_bits=a.eps_bits, algo=a.algo, log2_super=24, log2_N=15,
+                            fn=a.fn, start=a.start)
     import torch
 
     from paper_1211_3056_b200.device import DeviceSlice, FusedRunner
