@@ -248,6 +248,12 @@ def main():
     runner = FusedRunner(ds, algo, 1, 8, sub_cap=sub_cap, cand_cap=1 << 20)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
     stream = torch.cuda.current_stream()
+    runner.launch()
+    torch.cuda.synchronize()
+    c = runner.counts_host()
+    if c[1] > runner.sub_cap or c[2] > runner.cand_cap:  # size the outputs from the true counts
+        runner = FusedRunner(ds, algo, 1, 8, sub_cap=max(sub_cap, int(c[1]) + 1024),
+                             cand_cap=max(1 << 20, int(c[2]) + 1024))
     for _ in range(max(3, args.warmup)):
         runner.launch()
     torch.cuda.synchronize()
@@ -270,7 +276,7 @@ def main():
     iters = int(cnt.cpu().numpy().view(np.uint64)[3])
     phase_ms = None
     for _ in range(3):
-        r = run_phases(ds, algo, 1, 8, cand_hint=1 << 20)
+        r = run_phases(ds, algo, 1, 8, cand_hint=runner.cand_cap)
         phase_ms = list(r.phase_ms) if phase_ms is None else [min(a, b) for a, b in zip(phase_ms, r.phase_ms)]
     # ---- timed region: K steps, L2 flushed between steps, events on the stream
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]

@@ -61,7 +61,11 @@ int cuda_err(cudaError_t e, const char* where) {
 #ifndef HRB_P2_MINB
 #define HRB_P2_MINB 5
 #endif
-constexpr int NU = 16;             // domains per lane in phase 1 (stride-32 walk)
+#ifndef HRB_NU
+#define HRB_NU 16
+#endif
+constexpr int NU = HRB_NU;         // domains per lane in phase 1 (stride-32 walk), <= 32
+static_assert(NU >= 1 && NU <= 32, "a lane's verdicts live in one 32-bit word");
 constexpr int TILE = 32 * NU;      // domains per warp tile
 constexpr int CHUNK3 = 256;        // arguments per thread in phase 3
 constexpr int SCAN_BLOCKS = 592;   // 4 CTAs per SM on 148 SMs
