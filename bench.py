@@ -233,12 +233,19 @@ def main():
     from paper_1211_3056_b200 import _native as nat
     from paper_1211_3056_b200.device import DeviceSlice, FusedRunner, HostRunner, run_phases
 
-    torch.cuda.set_device(local)
+    # HRB_BENCH_ONE_DEVICE=1 runs every rank on cuda:0 over gloo: exercises the
+    # multi-rank partition / gather / max-over-ranks logic on a one-GPU box
+    one_dev = os.environ.get("HRB_BENCH_ONE_DEVICE") == "1"
+    dev_index = 0 if one_dev else local
+    torch.cuda.set_device(dev_index)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_dev:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     workers = max(1, (os.cpu_count() or 1) // max(1, int(os.environ.get("LOCAL_WORLD_SIZE", world))))
     batch, prep_s = prepare_rank(args, rank, world, workers)
     count = batch.arguments
@@ -280,7 +287,7 @@ def main():
         phase_ms = list(r.phase_ms) if phase_ms is None else [min(a, b) for a, b in zip(phase_ms, r.phase_ms)]
     # ---- timed region: K steps, L2 flushed between steps, events on the stream
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(dev_index)
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
@@ -324,7 +331,8 @@ def main():
                      for b, d, i in zip(bits, res.cand_dist.tolist(), res.cand_dom.tolist())],
                     dtype=np.uint64).reshape(-1, 4)
     local_res = ShardResult(np.array([counts[0], counts[1], counts[2], 0, counts[3], count], dtype=np.int64), cand)
-    t_all = torch.tensor([ms, float(np.mean(p1_ms)), e2e["ms_per_step"] if e2e else 0.0], device="cuda")
+    t_all = torch.tensor([ms, float(np.mean(p1_ms)), e2e["ms_per_step"] if e2e else 0.0],
+                         device="cpu" if one_dev else "cuda")
     gather_ms = 0.0
     if dist:
         dist.all_reduce(t_all, op=dist.ReduceOp.MAX)
@@ -387,7 +395,7 @@ def main():
             "host_polygen": {"seconds": prep_s, "workers": workers, "super_domains": batch.n_super,
                              "args_per_s": count / prep_s},
             "e2e": e2e}
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and world == 1:  # rank 0 at N=1 only
         cb = cpu_baseline(args, batch, args.cpu_seconds)
         cb["counts_match_gpu"] = cb.pop("counts") == [int(counts[0]), int(counts[1]), int(counts[2])]
         line["cpu_baseline"] = cb

@@ -58,6 +58,17 @@ int hrb_search_batch(int algo, int mode, int word_bits, int64_t n, const uint64_
                      void* stream);
 
 /*
+ * Regular-family verdicts only (Verdict, d, iterations; no points_placed):
+ * the throughput form the phases use (lockstep pairs, warp-uniform control
+ * flow), for callers that need what _run_search's callers read
+ * (pipeline.py:200-201, 228: `.success`).  algo must be HRB_ALGO_REGULAR or
+ * HRB_ALGO_REGULAR_UNROLLED (lowerbound.py:347-373); results equal
+ * hrb_search_batch's.  iterations may be NULL.
+ */
+int hrb_search_verdicts(int algo, int word_bits, int64_t n, const uint64_t* a, const uint64_t* b, const uint64_t* eps,
+                        const uint64_t* count, uint8_t* ok, uint64_t* d, uint64_t* iterations, void* stream);
+
+/*
  * hrb_search_batch plus the branch-decision stream of every problem: the
  * `trace` list the reference cores append to (lowerbound.py:109-110,
  * 126-127, 189-190, 246-259, 299-304), which its warp simulator consumes

@@ -27,6 +27,7 @@ EXPORTS = (
     "hrb_device_info",
     "hrb_search_batch",
     "hrb_search_trace",
+    "hrb_search_verdicts",
     "hrb_domain_coefficients",
     "hrb_phase1",
     "hrb_phase2",
@@ -88,6 +89,7 @@ def _declare(lib) -> None:
     lib.hrb_last_error.restype = C.c_char_p
     lib.hrb_device_info.argtypes = [I, C.c_char_p, I]
     lib.hrb_search_batch.argtypes = [I, I, I, I64, P, P, P, P, P, P, P, P, P, P]
+    lib.hrb_search_verdicts.argtypes = [I, I, I64, P, P, P, P, P, P, P, P]
     lib.hrb_search_trace.argtypes = [I, I, I, I64, P, P, P, P, P, P, P, P, P, P, I64, P, P]
     lib.hrb_domain_coefficients.argtypes = [C.POINTER(HrbSlice), P, P]
     lib.hrb_phase1.argtypes = [C.POINTER(HrbSlice), I, I, P, P, U64, P, P]

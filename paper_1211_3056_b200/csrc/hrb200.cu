@@ -321,6 +321,7 @@ struct WalkSrc {
         w->h0 = s1 + inc[1];
         return true;
     }
+    __device__ __forceinline__ void done(int, bool, uint64_t, uint32_t) {}
 };
 
 template <int W>
@@ -402,6 +403,7 @@ struct SubWalkSrc {
         t1 += dt1;
         return true;
     }
+    __device__ __forceinline__ void done(int, bool, uint64_t, uint32_t) {}
 };
 
 template <int W>
@@ -922,6 +924,59 @@ __global__ void __launch_bounds__(256) search_batch_kernel(int algo, int mode, i
     }
 }
 
+// Regular-family verdicts in the throughput form (tile_search.cuh): a warp
+// takes 32 * NU consecutive problems, lane l the problems l, l + 32, ...,
+// two in flight per lane in lockstep.  Counts >= 2^32 (outside the lockstep
+// form's 32-bit counters) run through the general core in place.
+template <int W>
+struct ArraySrc {
+    const uint64_t *a, *b, *eps, *cnt;
+    uint8_t* ok;
+    uint64_t *d, *it;
+    int64_t n, base;
+    bool unrolled;
+    __device__ __forceinline__ bool build(int k, uint64_t& av, uint64_t& bv, uint64_t& ev, uint32_t& N) {
+        const int64_t i = base + 32 * (int64_t)k;
+        if (i >= n) return false;
+        const uint64_t c = __ldg(&cnt[i]);
+        if (c >> 32) {
+            hrb::Outcome o = hrb::regular_search<W>(a[i], b[i], eps[i], c);
+            ok[i] = o.ok;
+            d[i] = o.d;
+            if (it) it[i] = unrolled ? (o.it + 1) >> 1 : o.it;
+            return false;
+        }
+        av = __ldg(&a[i]);
+        bv = __ldg(&b[i]);
+        ev = __ldg(&eps[i]);
+        N = (uint32_t)c;
+        return true;
+    }
+    __device__ __forceinline__ void done(int k, bool okv, uint64_t dv, uint32_t itv) {
+        const int64_t i = base + 32 * (int64_t)k;
+        ok[i] = okv;
+        d[i] = dv;
+        if (it) it[i] = itv;
+    }
+};
+
+template <int W>
+__global__ void __launch_bounds__(128, HRB_P1_MINB) search_verdict_kernel(int algo, int64_t n, const uint64_t* a,
+                                                                          const uint64_t* b, const uint64_t* eps,
+                                                                          const uint64_t* count, uint8_t* ok,
+                                                                          uint64_t* d, uint64_t* it) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t tiles = (n + TILE - 1) / TILE;
+    ArraySrc<W> src{a, b, eps, count, ok, d, it, n, 0, algo == hrb::ALGO_REGULAR_UNROLLED};
+    for (int64_t t = warp0; t < tiles; t += nwarps) {
+        src.base = t * TILE + lane;
+        unsigned long long its = 0;
+        hrb::lane_items<W, NU>(src, &its, src.unrolled);
+    }
+}
+
 // Same searches with the branch-decision stream of every problem recorded
 // (the reference cores' `trace` argument): bits LSB-first in
 // trace[i * wpp ...], the full decision count in trace_len[i] (decisions
@@ -1183,6 +1238,26 @@ int hrb_search_batch(int algo, int mode, int word_bits, int64_t n, const uint64_
     else if (reg) SB(32, true);
     else SB(32, false);
 #undef SB
+    CK(cudaGetLastError());
+    return HRB_OK;
+}
+
+int hrb_search_verdicts(int algo, int word_bits, int64_t n, const uint64_t* a, const uint64_t* b, const uint64_t* eps,
+                        const uint64_t* count, uint8_t* ok, uint64_t* d, uint64_t* iterations, void* stream) {
+    if (algo != hrb::ALGO_REGULAR && algo != hrb::ALGO_REGULAR_UNROLLED)
+        return set_err(HRB_ERR_CONFIG, "hrb_search_verdicts serves the regular family only");
+    if (word_bits != 32 && word_bits != 64) return set_err(HRB_ERR_CONFIG, "word_bits must be 32 or 64");
+    if (n < 0) return set_err(HRB_ERR_CONFIG, "negative batch size");
+    if (n == 0) return HRB_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t tiles = (n + TILE - 1) / TILE;
+    const int64_t blocks = (tiles * 32 + 127) / 128;
+    const int64_t cap = (int64_t)sm_count() * HRB_P1_MINB;
+    const int grid = (int)(blocks < cap ? blocks : cap);
+    if (word_bits == 64)
+        search_verdict_kernel<64><<<grid, 128, 0, st>>>(algo, n, a, b, eps, count, ok, d, iterations);
+    else
+        search_verdict_kernel<32><<<grid, 128, 0, st>>>(algo, n, a, b, eps, count, ok, d, iterations);
     CK(cudaGetLastError());
     return HRB_OK;
 }

@@ -64,6 +64,18 @@ __device__ __forceinline__ uint32_t qfix(uint64_t y, uint64_t x, int32_t k, uint
     return ku + (c ? 1u : 0u);
 }
 
+// floor(y/x + e) from the FP32 reciprocal in one round-down FFMA: with
+// M = 1.5 * 2^23, y*rcp + M rounded toward -inf lands on the integer grid of
+// [2^23, 2^24), i.e. M + floor(y*rcp) while y*rcp < 2^22.  The error of
+// y*rcp against y/x is |e| < 2^-21 y/x, so for y/x < 2^20 the result is
+// floor(y/x) except when y/x lies within |e| of an integer: then it can be
+// off by one either way, which the caller detects (remainder outside [0, x))
+// and repairs on its rare exact path.
+__device__ __forceinline__ int32_t qfloor(float yf, float rcp) {
+    const float kf = __fmaf_rd(yf, rcp, 12582912.0f);
+    return (int32_t)(__float_as_uint(kf) - 0x4B400000u);
+}
+
 __device__ __forceinline__ float rcp_approx(float x) {
     float r;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));  // <= 1 ulp
@@ -72,44 +84,34 @@ __device__ __forceinline__ float rcp_approx(float x) {
 
 constexpr int32_t QMAX = 1 << 20;
 
-// r -= S if r >= S; returns 1 if it subtracted (predicated IADD3 pair)
-__device__ __forceinline__ uint32_t csub(uint64_t& r, uint64_t S) {
-    uint32_t c;
-    asm("{\n\t.reg .pred p;\n\t"
-        "setp.ge.u64 p, %0, %2;\n\t"
-        "@p sub.u64 %0, %0, %2;\n\t"
-        "selp.u32 %1, 1, 0, p;\n\t}"
-        : "+l"(r), "=r"(c)
-        : "l"(S));
-    return c;
-}
-
 // One half-step, fast path: Lp = L mod S with its quotient k, and the
-// reduced d, from one FP32 reciprocal of S.  THEN selects the reference's
-// `p < q` body (d %= p) versus the `p >= q` body (d reduced past the new p;
-// when d < Lp, d < S already and the mod is the identity).  `big` flags a
-// quotient >= 2^20, where the estimate is not trusted (hs_exact redoes the
-// step).  Invariants on an active slot: S < L, d < L, S <= 2^63.
+// reduced d, from one FP32 reciprocal of S and round-down quotient estimates
+// that are exact except in rare near-integer cases.  THEN selects the
+// reference's `p < q` body (d %= p) versus the `p >= q` body (d reduced past
+// the new p; when d < Lp, d < S already and the mod is the identity).
+// `bad` flags a step the estimates may have got wrong -- a remainder outside
+// [0, S) or a quotient >= 2^20 -- which hs_exact redoes; nothing is fixed up
+// on the fast path.  Invariants on an active slot: S < L, d < L, S <= 2^63.
 template <bool THEN>
 __device__ __forceinline__ void hs_fast(uint64_t L, uint64_t S, float Lf, float Sf, uint64_t d, uint64_t& Lp,
-                                        uint64_t& dn, uint32_t& k, bool& big) {
+                                        uint64_t& dn, uint32_t& k, bool& bad) {
     const float rcp = rcp_approx(Sf);
-    const int32_t ke = qest(Lf, rcp);  // >= 0 because L > S
-    big = ke >= QMAX;
-    uint64_t r = L - (uint64_t)(uint32_t)ke * S;
-    k = (uint32_t)ke + csub(r, S);
+    const int32_t ke = qfloor(Lf, rcp);  // floor(L/S) >= 1, estimate >= 0
+    const uint64_t r = L - (uint64_t)(uint32_t)ke * S;
     uint64_t x = d;
-    if (!THEN) csub(x, r);
-    // quotient of x by S is >= 0, so the estimate is >= -1 (clamped to 0,
-    // where x < S already holds)
-    const uint32_t ke2 = (uint32_t)max(qest(__ull2float_rn(x), rcp), 0);
-    uint64_t y = x - (uint64_t)ke2 * S;
-    csub(y, S);
+    if (!THEN && x >= r) x -= r;
+    // the quotient of x by S is >= 0; an estimate of -1 (x/S within |e| of
+    // 0 from above) is clamped to 0, which is then exact
+    const uint32_t ke2 = (uint32_t)max(qfloor(__ull2float_rn(x), rcp), 0);
+    const uint64_t y = x - (uint64_t)ke2 * S;
+    bad = (ke >= QMAX) | (r >= S) | (y >= S);
     Lp = r;
     dn = y;
+    k = (uint32_t)ke;
 }
 
-// The same half-step with hardware 64-bit division (rare: quotient >= 2^20).
+// The same half-step with hardware 64-bit division (rare: a quotient >= 2^20
+// or an estimate that missed by one).
 // k saturates at 2^32 - 1: any quotient that large ends the search (cS >= 1
 // makes cLp >= 2^32 - 1 >= N - cS), exactly as the reference's u + v >= N.
 // Out of line and by value, so the hot loop keeps its registers.
@@ -184,15 +186,17 @@ __device__ __forceinline__ void pair_step(Slot& s0, Slot& s1, uint32_t n0, uint3
 // otherwise `s` holds the state before the first else-half (A < B).
 template <int W>
 __device__ __forceinline__ bool reg_start(uint64_t a, uint64_t b, uint64_t eps, uint32_t N, Slot& s, bool* ok,
-                                          uint32_t* it) {
+                                          uint32_t* it, uint64_t* dout) {
     if (b < eps) {
         *ok = false;
         *it = 0;
+        *dout = b;
         return true;
     }
     if (a == 0 || N <= 1) {
         *ok = b > eps;
         *it = 0;
+        *dout = b;
         return true;
     }
     // k = one / a, rem = one mod a (one = 2^W); the quotient is >= 1 since a < one
@@ -219,6 +223,7 @@ __device__ __forceinline__ bool reg_start(uint64_t a, uint64_t b, uint64_t eps, 
         if (W == 64 && a == 1) {  // k = 2^64: q -> 0, d = 0, exhausted
             *ok = false;
             *it = 1;
+            *dout = 0;
             return true;
         }
         if (W == 64) {
@@ -234,6 +239,7 @@ __device__ __forceinline__ bool reg_start(uint64_t a, uint64_t b, uint64_t eps, 
     if (rem == 0 || k >= (uint64_t)N - 1) {
         *ok = d > eps;
         *it = 1;
+        *dout = d;
         return true;
     }
     s.A = rem;  // divisor of the first else-half
@@ -249,6 +255,8 @@ __device__ __forceinline__ bool reg_start(uint64_t a, uint64_t b, uint64_t eps, 
 // All items of one lane, two searches at a time in lockstep.
 //   src.build(k, a, b, eps, N) builds item k; called for k = 0, 1, 2, ... in
 //   order, exactly once each; returns false for an invalid item.
+//   src.done(k, ok, d, iterations) reports each valid item's outcome (the
+//   phase kernels ignore it; the verdict batch stores it).
 // Returns the lane's failure bits (bit k = item k failed) and adds the
 // items' iteration counts (halved and rounded up for the unrolled variant)
 // to *iters.
@@ -267,18 +275,21 @@ __device__ __forceinline__ uint32_t lane_items(Src& src, unsigned long long* ite
         uint64_t a, b, e0 = 0, e1 = 0;
         uint32_t n0 = 0, n1 = 0, it;
         bool ok, act0 = false, act1 = false;
+        uint64_t d_early;
         if (src.build(k, a, b, e0, n0)) {
-            if (reg_start<W>(a, b, e0, n0, s0, &ok, &it)) {
+            if (reg_start<W>(a, b, e0, n0, s0, &ok, &it, &d_early)) {
                 its += halve ? (it + 1) >> 1 : it;
                 fails |= ok ? 0u : 1u << k;
+                src.done(k, ok, d_early, halve ? (it + 1) >> 1 : it);
             } else {
                 act0 = true;
             }
         }
         if (src.build(k + 1, a, b, e1, n1)) {
-            if (reg_start<W>(a, b, e1, n1, s1, &ok, &it)) {
+            if (reg_start<W>(a, b, e1, n1, s1, &ok, &it, &d_early)) {
                 its += halve ? (it + 1) >> 1 : it;
                 fails |= ok ? 0u : 2u << k;
+                src.done(k + 1, ok, d_early, halve ? (it + 1) >> 1 : it);
             } else {
                 act1 = true;
             }
@@ -299,11 +310,13 @@ __device__ __forceinline__ uint32_t lane_items(Src& src, unsigned long long* ite
             if (act0 && f0) {
                 its += halve ? (h + 1) >> 1 : h;
                 fails |= (s0.d > e0) ? 0u : 1u << k;
+                src.done(k, s0.d > e0, s0.d, halve ? (h + 1) >> 1 : h);
                 act0 = false;
             }
             if (act1 && f1) {
                 its += halve ? (h + 1) >> 1 : h;
                 fails |= (s1.d > e1) ? 0u : 2u << k;
+                src.done(k + 1, s1.d > e1, s1.d, halve ? (h + 1) >> 1 : h);
                 act1 = false;
             }
             pair_step<true>(s0, s1, n0, n1, act0, act1, f0, f1);
@@ -311,11 +324,13 @@ __device__ __forceinline__ uint32_t lane_items(Src& src, unsigned long long* ite
             if (act0 && f0) {
                 its += halve ? (h + 1) >> 1 : h;
                 fails |= (s0.d > e0) ? 0u : 1u << k;
+                src.done(k, s0.d > e0, s0.d, halve ? (h + 1) >> 1 : h);
                 act0 = false;
             }
             if (act1 && f1) {
                 its += halve ? (h + 1) >> 1 : h;
                 fails |= (s1.d > e1) ? 0u : 2u << k;
+                src.done(k + 1, s1.d > e1, s1.d, halve ? (h + 1) >> 1 : h);
                 act1 = false;
             }
         }

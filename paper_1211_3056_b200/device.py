@@ -311,3 +311,22 @@ def search_trace_arrays(algo_code: int, mode_code: int, word_bits: int, a, b, ep
     bits = np.unpackbits(words.cpu().numpy().view(np.uint8).reshape(m, wpp * 8), axis=1, bitorder="little")
     traces = [bits[i, : lens[i]].astype(bool).tolist() for i in range(n)]
     return (ok[:n].cpu().numpy(), _u64(d[:n]), _u64(it[:n]), _u64(pl[:n]), ph[:n].cpu().numpy(), traces)
+
+
+def search_verdict_arrays(algo_code: int, word_bits: int, a, b, eps, count, device=None):
+    """hrb_search_verdicts over host arrays (regular family): the lockstep
+    throughput form; returns host arrays (ok, d, iterations)."""
+    torch = nat.require_cuda()
+    lib = nat.load()
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    n = len(a)
+    ins = [torch.from_numpy(np.ascontiguousarray(np.asarray(x, dtype=np.uint64)).view(np.int64)).to(dev)
+           for x in (a, b, eps, count)]
+    ok = torch.empty(max(n, 1), dtype=torch.uint8, device=dev)
+    d = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+    it = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+    nat.check("hrb_search_verdicts", lib.hrb_search_verdicts(algo_code, word_bits, n, *(x.data_ptr() for x in ins),
+                                                             ok.data_ptr(), d.data_ptr(), it.data_ptr(),
+                                                             nat.stream_ptr()))
+    torch.cuda.synchronize()
+    return ok[:n].cpu().numpy(), _u64(d[:n]), _u64(it[:n])

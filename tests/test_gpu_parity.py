@@ -262,3 +262,75 @@ def test_large_slice_logical_shards_and_rerun_are_identical():
         cands.append(rr.cand_index)
     assert np.array_equal(np.concatenate(fails), a.fail_ids)
     assert np.array_equal(np.concatenate(cands), a.cand_index)
+
+
+def _adversarial_problems(rng, n):
+    """Inputs that stress the lockstep form's rare paths: huge and
+    near-integer continued-fraction quotients (a close to a rational with a
+    small denominator, tiny a, a near 1), counts at the 32-bit edge."""
+    one = 1 << 64
+    rows = []
+    for k in range(n):
+        kind = k % 8
+        if kind == 0:    # a ~ one * p / q: the expansion hits a huge quotient
+            q = int(rng.integers(2, 5000))
+            p = int(rng.integers(1, q))
+            a = (one * p // q + int(rng.integers(-3, 4))) % one
+        elif kind == 1:  # tiny slope
+            a = int(rng.integers(1, 1 << 20))
+        elif kind == 2:  # slope just below one
+            a = one - int(rng.integers(1, 1 << 20))
+        elif kind == 3:  # near 2^64 / k
+            a = one // int(rng.integers(2, 1 << 16)) + int(rng.integers(-2, 3))
+        elif kind == 4:  # near 2^63 (S <= 2^63 boundary)
+            a = (1 << 63) + int(rng.integers(-1 << 10, 1 << 10))
+        else:
+            a = int(rng.integers(0, 1 << 63)) * 2 + int(rng.integers(0, 2))
+        a %= one
+        b = int(rng.integers(0, 1 << 63)) * 2 + int(rng.integers(0, 2))
+        e = int(rng.integers(1, 1 << 40))
+        N = [1, 2, 3, 1 << 12, 1 << 15, (1 << 32) - 1, 1 << 32, (1 << 32) + 7][int(rng.integers(0, 8))]
+        rows.append((a, b, e, N))
+    return [np.array([r[i] for r in rows], dtype=np.uint64) for i in range(4)]
+
+
+@pytest.mark.parametrize("algo", ["regular", "regular_unrolled"])
+@pytest.mark.parametrize("kind", ["random", "adversarial", "grid"])
+def test_search_verdicts_lockstep_form_vs_oracle(algo, kind):
+    """hrb_search_verdicts (the phases' lockstep form: round-down FP32
+    quotient estimates, exact path entered by warp vote) equals the oracle
+    port of _regular_core / _regular_unrolled_core on (verdict, d, it)."""
+    from paper_1211_3056_b200.device import search_verdict_arrays
+
+    rng = np.random.default_rng(99 + (algo == "regular_unrolled") + 7 * ["random", "adversarial", "grid"].index(kind))
+    W = 64
+    if kind == "random":
+        n = 1 << 21
+        a = rng.integers(0, 2**64, n, dtype=np.uint64)
+        b = rng.integers(0, 2**64, n, dtype=np.uint64)
+        e = rng.integers(1, 2**40, n, dtype=np.uint64)
+        N = rng.choice(np.array([1, 2, 17, 1 << 12, 1 << 15, 1 << 20, (1 << 31) + 5], dtype=np.uint64), n)
+    elif kind == "adversarial":
+        a, b, e, N = _adversarial_problems(rng, 1 << 17)
+    else:  # criterion-2 grid embedded << 54
+        grid = 1 << 10
+        A, B = np.meshgrid(np.arange(grid, dtype=np.uint64), np.arange(grid, dtype=np.uint64), indexing="ij")
+        a, b = A.ravel() << np.uint64(54), B.ravel() << np.uint64(54)
+        e = np.full(a.size, (grid >> 6) << 54, dtype=np.uint64)
+        N = np.full(a.size, 1024, dtype=np.uint64)
+    ok, d, it = search_verdict_arrays(ALGO_CODE[algo], W, a, b, e, N)
+    wok, wd, wit, _, _ = oracle.search_batch(algo, 1, 1 << 64, a, b, e, N)
+    bad = np.nonzero((ok != wok) | (d != wd) | (it != wit))[0]
+    assert bad.size == 0, [(int(a[k]), int(b[k]), int(e[k]), int(N[k])) for k in bad[:3]]
+
+
+def test_search_verdicts_w32_vs_reference_goldens():
+    from paper_1211_3056_b200.device import search_verdict_arrays
+
+    g = load_search("search_w32.npz")
+    for col, (algo, mode) in enumerate(CORE_COLUMNS):
+        if not algo.startswith("regular"):
+            continue
+        ok, d, it = search_verdict_arrays(ALGO_CODE[algo], 32, g["a"], g["b"], g["eps"], g["count"])
+        assert np.array_equal(ok, g["ok"][:, col]) and np.array_equal(d, g["d"][:, col])
+        assert np.array_equal(it, g["it"][:, col])
