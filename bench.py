@@ -251,16 +251,18 @@ def main():
     count = batch.arguments
     algo = 2 if args.algo == "regular" else 0
     ds = DeviceSlice(batch)
-    sub_cap = max(1 << 16, batch.n_total * 2)
+    sub_cap = max(1 << 16, batch.n_total // 8)  # grown below from the true count if needed
     runner = FusedRunner(ds, algo, 1, 8, sub_cap=sub_cap, cand_cap=1 << 20)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
     stream = torch.cuda.current_stream()
-    runner.launch()
-    torch.cuda.synchronize()
-    c = runner.counts_host()
-    if c[1] > runner.sub_cap or c[2] > runner.cand_cap:  # size the outputs from the true counts
-        runner = FusedRunner(ds, algo, 1, 8, sub_cap=max(sub_cap, int(c[1]) + 1024),
-                             cand_cap=max(1 << 20, int(c[2]) + 1024))
+    while True:  # size the outputs from the true counts (a truncated phase 2 undercounts phase 3)
+        runner.launch()
+        torch.cuda.synchronize()
+        c = runner.counts_host()
+        if c[1] <= runner.sub_cap and c[2] <= runner.cand_cap:
+            break
+        runner = FusedRunner(ds, algo, 1, 8, sub_cap=max(runner.sub_cap, int(c[1]) + 1024),
+                             cand_cap=max(runner.cand_cap, int(c[2]) + 1024))
     for _ in range(max(3, args.warmup)):
         runner.launch()
     torch.cuda.synchronize()

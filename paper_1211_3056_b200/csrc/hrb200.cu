@@ -67,7 +67,12 @@ int cuda_err(cudaError_t e, const char* where) {
 constexpr int NU = HRB_NU;         // domains per lane in phase 1 (stride-32 walk), <= 32
 static_assert(NU >= 1 && NU <= 32, "a lane's verdicts live in one 32-bit word");
 constexpr int TILE = 32 * NU;      // domains per warp tile
-constexpr int CHUNK3 = 256;        // arguments per thread in phase 3
+// Phase-3 arguments per thread: chosen on the device per launch (meta[2])
+// between CHUNK3_MIN and CHUNK3_MAX (powers of two, multiples of 32): the
+// largest chunk that still gives every SM enough threads (fewer per-item
+// setups when phase 2 left many subdomains, more parallelism when it left few).
+constexpr int CHUNK3_MIN = 128;
+constexpr int CHUNK3_MAX = 2048;
 constexpr int SCAN_BLOCKS = 592;   // 4 CTAs per SM on 148 SMs
 constexpr int SCAN_THREADS = 256;
 
@@ -526,39 +531,50 @@ struct Cand {
     uint32_t rank;
 };
 
-// 96-bit lane registers for the phase-3 walk: value = (h << 64) + (m << 32),
-// the low 32 bits being the (zero) bits below the 2^-F grid once shifted by
-// sh = 128 - F >= 32.  V += D1 is one ALU add chain (IADD3 + 2 IADD3.X);
-// D1 += D2 is issued as IMAD-with-carry so it runs on the FMA pipe and the
-// two chains overlap (the walk is otherwise ALU-pipe bound).
+// 96-bit lane registers for the phase-3 walk: value = (h1 << 96) + (h0 << 64)
+// + (m << 32), the low 32 bits being the (zero) bits below the 2^-F grid once
+// shifted by sh = 128 - F >= 32.  Three separate 32-bit words, so no 64-bit
+// packing instructions appear in the walk.  V += D1 is one ALU add chain
+// (IADD3 + 2 IADD3.X); D1 += D2 is issued as IMAD-with-carry so it runs on
+// the FMA pipe and the two chains overlap.
 struct R96 {
-    uint32_t m;
-    uint64_t h;
+    uint32_t m, h0, h1;
 };
 
 __device__ __forceinline__ R96 r96_of(u128 x) {
     R96 r;
     r.m = (uint32_t)(x >> 32);
-    r.h = (uint64_t)(x >> 64);
+    r.h0 = (uint32_t)(x >> 64);
+    r.h1 = (uint32_t)(x >> 96);
     return r;
 }
 
-__device__ __forceinline__ u128 u128_of(R96 r) { return ((u128)r.h << 64) | ((u128)r.m << 32); }
+__device__ __forceinline__ u128 u128_of(R96 r) {
+    return ((u128)r.h1 << 96) | ((u128)r.h0 << 64) | ((u128)r.m << 32);
+}
 
 __device__ __forceinline__ void add96_alu(R96& x, const R96& y) {
-    uint32_t h0 = (uint32_t)x.h, h1 = (uint32_t)(x.h >> 32);
     asm("add.cc.u32 %0, %0, %3;\n\taddc.cc.u32 %1, %1, %4;\n\taddc.u32 %2, %2, %5;"
-        : "+r"(x.m), "+r"(h0), "+r"(h1)
-        : "r"(y.m), "r"((uint32_t)y.h), "r"((uint32_t)(y.h >> 32)));
-    x.h = ((uint64_t)h1 << 32) | h0;
+        : "+r"(x.m), "+r"(x.h0), "+r"(x.h1)
+        : "r"(y.m), "r"(y.h0), "r"(y.h1));
 }
 
 __device__ __forceinline__ void add96_fma(R96& x, const R96& y) {
-    uint32_t h0 = (uint32_t)x.h, h1 = (uint32_t)(x.h >> 32);
     asm("mad.lo.cc.u32 %0, %3, 1, %0;\n\tmadc.lo.cc.u32 %1, %4, 1, %1;\n\tmadc.lo.u32 %2, %5, 1, %2;"
-        : "+r"(x.m), "+r"(h0), "+r"(h1)
-        : "r"(y.m), "r"((uint32_t)y.h), "r"((uint32_t)(y.h >> 32)));
-    x.h = ((uint64_t)h1 << 32) | h0;
+        : "+r"(x.m), "+r"(x.h0), "+r"(x.h1)
+        : "r"(y.m), "r"(y.h0), "r"(y.h1));
+}
+
+// meta[2] <- the phase-3 chunk for this launch: halve from CHUNK3_MAX while
+// the item count (subdomains x chunks per subdomain) stays below min_items.
+__global__ void chunk3_kernel(unsigned long long* meta, const uint64_t* sub_count, uint64_t sub_cap,
+                              uint64_t min_items) {
+    uint64_t ns = *sub_count;
+    if (ns > sub_cap) ns = sub_cap;
+    const uint64_t maxstep = meta[1];
+    uint64_t chunk = CHUNK3_MAX;
+    while (chunk > CHUNK3_MIN && ns * ((maxstep + chunk - 1) / chunk) < min_items) chunk >>= 1;
+    meta[2] = chunk;
 }
 
 // Phase 3 walk, scaled form: with sh = 128 - F the registers hold
@@ -578,6 +594,7 @@ __global__ void __launch_bounds__(256) phase3_kernel(SliceDev s, int split, cons
                                                      uint64_t app_cap) {
     const int lane = threadIdx.x & 31;
     const uint64_t maxstep = meta[1];
+    const uint32_t CHUNK3 = (uint32_t)meta[2];
     const uint64_t CH = (maxstep + CHUNK3 - 1) / CHUNK3;
     uint64_t ns = *sub_count;
     if (ns > sub_cap) ns = sub_cap;
@@ -621,15 +638,17 @@ __global__ void __launch_bounds__(256) phase3_kernel(SliceDev s, int split, cons
             }
         }
         const uint64_t Khi = (uint64_t)(K >> 64);
+        const uint32_t Ktop = (uint32_t)(K >> 96);
         uint32_t rank = 0;
         R96 v96 = r96_of(V), d96 = r96_of(D1), e96 = r96_of(D2);
         for (uint32_t x0 = 0; x0 < CHUNK3; x0 += 32) {
             const u128 V0 = NARROW ? u128_of(v96) : V, D10 = NARROW ? u128_of(d96) : D1;
             bool any = false;
+            uint32_t lo_top = 0xFFFFFFFFu;  // min of the top words over the 32 arguments (one VIMNMX each)
 #pragma unroll 16
             for (uint32_t x = 0; x < 32; x++) {
                 if (NARROW) {
-                    any |= v96.h <= Khi;  // conservative: V < K implies hi(V) <= hi(K)
+                    lo_top = min(lo_top, v96.h1);  // conservative: V < K implies top32(V) <= top32(K)
                     add96_alu(v96, d96);
                     add96_fma(d96, e96);
                 } else {
@@ -638,6 +657,7 @@ __global__ void __launch_bounds__(256) phase3_kernel(SliceDev s, int split, cons
                     D1 += D2;
                 }
             }
+            if (NARROW) any = lo_top <= Ktop;
             if (__any_sync(0xffffffffu, any)) {  // rare: re-walk exactly and append in order
                 u128 v = V0, d = D10;
                 for (uint32_t x = 0; x < 32; x++) {
@@ -748,7 +768,7 @@ struct P3Offsets {  // per-item candidate counts -> per-item output offsets
     __device__ uint64_t size() const {
         uint64_t ns = *sub_count;
         if (ns > sub_cap) ns = sub_cap;
-        return ns * ((meta[1] + CHUNK3 - 1) / CHUNK3);
+        return ns * ((meta[1] + meta[2] - 1) / meta[2]);
     }
     __device__ uint32_t count(uint64_t i) const { return counts[i]; }
     __device__ void emit(uint64_t i, uint64_t off) const { offs[i] = off; }
@@ -1158,8 +1178,14 @@ int phase3_impl(Workspace& ws, const hrb_slice* s, const SliceDev& sd, int split
                 uint64_t* cdom, uint64_t* cand_count, uint64_t cap, cudaStream_t st) {
     int rc;
     const uint64_t maxstep = s->max_dom_n;  // >= every subdomain step
-    const uint64_t CH = (maxstep + CHUNK3 - 1) / CHUNK3;
-    const uint64_t items = sub_cap * (CH ? CH : 1);
+    // items <= max(2 min_items, sub_cap * chunks of the largest size) by the
+    // chunk rule of chunk3_kernel
+    const uint64_t min_items = (uint64_t)sm_count() * 2048;
+    const uint64_t CH = (maxstep + CHUNK3_MAX - 1) / CHUNK3_MAX;
+    const uint64_t ch_min = (maxstep + CHUNK3_MIN - 1) / CHUNK3_MIN;
+    uint64_t items = sub_cap * (CH ? CH : 1);
+    items = items > 2 * min_items + sub_cap ? items : 2 * min_items + sub_cap;
+    if (items > sub_cap * ch_min) items = sub_cap * ch_min;
     if ((rc = ws.counts3.ensure(sizeof(uint32_t) * (items + 1)))) return rc;
     if ((rc = ws.offs3.ensure(sizeof(uint64_t) * (items + 1)))) return rc;
     const uint64_t app_cap = cap;
@@ -1172,6 +1198,7 @@ int phase3_impl(Workspace& ws, const hrb_slice* s, const SliceDev& sd, int split
         sub_t = (const uint32_t*)ws.sub_t.p;
     }
     CK(cudaMemsetAsync(ws.appc.p, 0, sizeof(unsigned long long), st));
+    chunk3_kernel<<<1, 1, 0, st>>>((unsigned long long*)ws.meta.p, sub_count, sub_cap, min_items);
     const int grid = sm_count() * 8;
     if (sd.F <= 96)
         phase3_kernel<true><<<grid, 256, 0, st>>>(sd, split, sub_keys, sub_t, sub_count, sub_cap,
@@ -1425,7 +1452,7 @@ int hrb_run_slice_host(const hrb_slice* hs, int algo, int mode, int split, uint6
     ds.last_n = (const uint32_t*)H.ln.p;
     ds.dom_base = (const uint64_t*)H.db.p;
     ds.m0 = (const uint64_t*)H.m0.p;
-    uint64_t sub_cap = (uint64_t)NT * 2 + 1024;
+    uint64_t sub_cap = (uint64_t)NT / 8 + 1024;  // grown once from the true count
     const uint64_t fcap = (uint64_t)NT;
     for (int attempt = 0; attempt < 2; attempt++) {
         if ((rc = H.fail.ensure(sizeof(uint64_t) * (fcap + 1))) || (rc = H.sub.ensure(sizeof(uint64_t) * (sub_cap + 1))) ||
