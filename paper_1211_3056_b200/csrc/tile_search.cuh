@@ -2,13 +2,15 @@
 //
 // A warp owns a tile of 32*NU work items (lane l takes items l, l+32, ...).
 // Each lane advances TWO searches in lockstep (items k and k+1): two
-// independent dependency chains per thread hide the FP64 / conversion
-// latencies of the quotient estimate, while the regular algorithm's nearly
+// independent dependency chains per thread hide the MUFU / conversion
+// latencies of the quotient estimates, while the regular algorithm's nearly
 // constant iteration count (NMDM 0.1%) keeps the 64
 // searches of a warp in step.  Each half-step is straight-line code: the
-// role swap is unconditional (so the compiler renames instead of moving),
-// the d-reduction offset is a select, and the only branches are one rarely
-// taken exact-division fallback and the loop exit.
+// (p, q) roles alternate between two fixed registers, quotients come from
+// one FP32 reciprocal with round-down estimates, and every correction (a
+// near-integer estimate, a quotient >= 2^20, the first step's divisor above
+// 2^63) is taken by the whole warp on one vote-gated exact path; the loop
+// branches are warp-uniform.
 //
 // Restates _regular_core (lowerbound.py:228-267) bit-exactly for the
 // verdict, d and the iteration count, for counts N < 2^32 (always true on
@@ -19,15 +21,6 @@
 #include "search_core.cuh"
 
 namespace hrb {
-
-constexpr double TWO32 = 4294967296.0;
-
-__device__ __forceinline__ double rcp_refined(double xd) {
-    double r;
-    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(xd));
-    double e = fma(-xd, r, 1.0);
-    return fma(r, e, r);
-}
 
 // One search in flight.  The reference's (p, q) pair lives in two fixed
 // registers A, B whose roles alternate: before each else-half A is the
@@ -41,28 +34,6 @@ struct Slot {
     float Af, Bf;
     uint32_t cA, cB;
 };
-
-// Quotient estimate from the FP32 reciprocal: with M = 1.5 * 2^23 the FFMA
-// y*rcp(x) + (M - 1) lands in [2^23, 2^24) where floats are the integers, so
-// its single rounding IS round-to-nearest(y/x - 1 + e) with |e| < 2^-22 y/x;
-// for y/x < 2^20 that is floor(y/x) or floor(y/x) - 1 (possibly -1 when the
-// quotient is 0), read straight from the bit pattern -- no F2I on the
-// conversion pipe.  Quotients >= 2^20 are reported for the exact path.
-__device__ __forceinline__ int32_t qest(float yf, float rcp) {
-    const float kf = fmaf(yf, rcp, 12582911.0f);  // 1.5 * 2^23 - 1
-    return (int32_t)(__float_as_uint(kf) - 0x4B400000u);
-}
-
-// r = y - k x with k in {K-1, K} (K = floor(y/x)), fixed to the exact
-// remainder; returns the exact quotient.  k = -1 (K = 0) is clamped to 0,
-// where y < x already holds, so the products stay unsigned 32x64.
-__device__ __forceinline__ uint32_t qfix(uint64_t y, uint64_t x, int32_t k, uint64_t& r) {
-    const uint32_t ku = (uint32_t)max(k, 0);
-    const uint64_t rr = y - (uint64_t)ku * x;
-    const bool c = rr >= x;
-    r = c ? rr - x : rr;
-    return ku + (c ? 1u : 0u);
-}
 
 // floor(y/x + e) from the FP32 reciprocal in one round-down FFMA: with
 // M = 1.5 * 2^23, y*rcp + M rounded toward -inf lands on the integer grid of
@@ -92,11 +63,17 @@ constexpr int32_t QMAX = 1 << 20;
 // `bad` flags a step the estimates may have got wrong -- a remainder outside
 // [0, S) or a quotient >= 2^20 -- which hs_exact redoes; nothing is fixed up
 // on the fast path.  Invariants on an active slot: S < L, d < L, S <= 2^63.
-template <bool THEN>
+//
+// FIRST: the first step of a search, the only one whose divisor (a) may
+// exceed 2^63 and whose dividend (one - a) may be below it.  Its quotient
+// estimate is clamped at 0 and a wrapped subtraction is caught directly
+// (result above its minuend), since ">= S" no longer implies a wrap there.
+template <bool THEN, bool FIRST = false>
 __device__ __forceinline__ void hs_fast(uint64_t L, uint64_t S, float Lf, float Sf, uint64_t d, uint64_t& Lp,
                                         uint64_t& dn, uint32_t& k, bool& bad) {
     const float rcp = rcp_approx(Sf);
-    const int32_t ke = qfloor(Lf, rcp);  // floor(L/S) >= 1, estimate >= 0
+    // floor(L/S) >= 1 except on a first step, so the estimate is >= 0
+    const int32_t ke = FIRST ? max(qfloor(Lf, rcp), 0) : qfloor(Lf, rcp);
     const uint64_t r = L - (uint64_t)(uint32_t)ke * S;
     uint64_t x = d;
     if (!THEN && x >= r) x -= r;
@@ -105,6 +82,7 @@ __device__ __forceinline__ void hs_fast(uint64_t L, uint64_t S, float Lf, float 
     const uint32_t ke2 = (uint32_t)max(qfloor(__ull2float_rn(x), rcp), 0);
     const uint64_t y = x - (uint64_t)ke2 * S;
     bad = (ke >= QMAX) | (r >= S) | (y >= S);
+    if (FIRST) bad |= (r > L) | (y > x);
     Lp = r;
     dn = y;
     k = (uint32_t)ke;
@@ -148,7 +126,9 @@ __device__ __forceinline__ bool hs_commit(uint64_t& L, float& Lf, uint32_t& cL, 
 // the then-half A by B.  Must be called by all 32 lanes of the warp
 // (warp-uniform control flow): the rare exact path is entered by the whole
 // warp through one vote, so the hot path carries no divergent branch.
-template <bool THEN>
+//
+// FIRST marks the first then-half of a search (see hs_fast).
+template <bool THEN, bool FIRST = false>
 __device__ __forceinline__ void pair_step(Slot& s0, Slot& s1, uint32_t n0, uint32_t n1, bool act0, bool act1,
                                           bool& f0, bool& f1) {
     uint64_t& L0 = THEN ? s0.A : s0.B;
@@ -163,8 +143,8 @@ __device__ __forceinline__ void pair_step(Slot& s0, Slot& s1, uint32_t n0, uint3
     uint64_t Lp0, dn0, Lp1, dn1;
     uint32_t k0, k1;
     bool b0, b1;
-    hs_fast<THEN>(L0, S0, Lf0, Sf0, s0.d, Lp0, dn0, k0, b0);
-    hs_fast<THEN>(L1, S1, Lf1, Sf1, s1.d, Lp1, dn1, k1, b1);
+    hs_fast<THEN, FIRST>(L0, S0, Lf0, Sf0, s0.d, Lp0, dn0, k0, b0);
+    hs_fast<THEN, FIRST>(L1, S1, Lf1, Sf1, s1.d, Lp1, dn1, k1, b1);
     b0 = b0 && act0;
     b1 = b1 && act1;
     if (__any_sync(0xffffffffu, b0 || b1)) {
@@ -181,73 +161,32 @@ __device__ __forceinline__ void pair_step(Slot& s0, Slot& s1, uint32_t n0, uint3
     f1 = hs_commit(L1, Lf1, cL1, cS1, s1.d, n1, Lp1, dn1, k1);
 }
 
-// _regular_core up to and including the first (then-) half-step against
-// one = 2^W.  Returns true if the search ended there (*ok, *it set);
-// otherwise `s` holds the state before the first else-half (A < B).
+// Set up a slot for _regular_core (lowerbound.py:228-267).  Returns true if
+// the search ends before its loop (b < eps; a == 0 or N <= 1: 0 iterations)
+// with *ok, *dout set.  Otherwise the slot holds (one - a, a) with counts
+// (1, 1): its first then-half divides one - a by a, which yields the
+// reference's first quotient floor(one / a) minus one, the count k + 1 and
+// the remainder one mod a -- the whole first iteration on the lockstep path
+// (no 65-bit `one` needed).
 template <int W>
-__device__ __forceinline__ bool reg_start(uint64_t a, uint64_t b, uint64_t eps, uint32_t N, Slot& s, bool* ok,
-                                          uint32_t* it, uint64_t* dout) {
+__device__ __forceinline__ bool slot_init(uint64_t a, uint64_t b, uint64_t eps, uint32_t N, Slot& s, bool* ok,
+                                          uint64_t* dout) {
     if (b < eps) {
         *ok = false;
-        *it = 0;
         *dout = b;
         return true;
     }
     if (a == 0 || N <= 1) {
         *ok = b > eps;
-        *it = 0;
         *dout = b;
         return true;
     }
-    // k = one / a, rem = one mod a (one = 2^W); the quotient is >= 1 since a < one
-    const double ad = __ull2double_rn(a);
-    const double inv = rcp_refined(ad);
-    const double kd = fma(W == 64 ? 18446744073709551616.0 : 4294967296.0, inv, -0.5);
-    uint64_t k, rem, d;
-    if (kd < TWO32) {
-        uint32_t k0 = __double2uint_rz(kd);
-        k0 = k0 ? k0 : 1u;
-        rem = (W == 64) ? (0ull - (uint64_t)k0 * a) : ((1ull << 32) - (uint64_t)k0 * a);
-        const bool c = rem >= a;
-        rem = c ? rem - a : rem;
-        k = k0 + (c ? 1u : 0u);
-        const double kd2 = fma(__ull2double_rn(b), inv, -0.5);
-        if (kd2 < TWO32) {
-            const uint32_t k2 = __double2uint_rz(kd2);
-            d = b - (uint64_t)k2 * a;
-            d = d >= a ? d - a : d;
-        } else {
-            d = b % a;
-        }
-    } else {
-        if (W == 64 && a == 1) {  // k = 2^64: q -> 0, d = 0, exhausted
-            *ok = false;
-            *it = 1;
-            *dout = 0;
-            return true;
-        }
-        if (W == 64) {
-            const uint64_t k0 = ~0ull / a, r0 = ~0ull - k0 * a;
-            k = (r0 == a - 1) ? k0 + 1 : k0;
-            rem = (r0 == a - 1) ? 0 : r0 + 1;
-        } else {
-            k = (1ull << 32) / a;
-            rem = (1ull << 32) - k * a;
-        }
-        d = b % a;
-    }
-    if (rem == 0 || k >= (uint64_t)N - 1) {
-        *ok = d > eps;
-        *it = 1;
-        *dout = d;
-        return true;
-    }
-    s.A = rem;  // divisor of the first else-half
+    s.A = (W == 64) ? (0ull - a) : ((1ull << 32) - a);
     s.B = a;
-    s.d = d;
-    s.Af = __ull2float_rn(rem);
+    s.d = b;
+    s.Af = __ull2float_rn(s.A);
     s.Bf = __ull2float_rn(a);
-    s.cA = (uint32_t)k;
+    s.cA = 1;
     s.cB = 1;
     return false;
 }
@@ -273,23 +212,21 @@ __device__ __forceinline__ uint32_t lane_items(Src& src, unsigned long long* ite
     for (int k = 0; k < kend; k += 2) {
         Slot s0, s1;
         uint64_t a, b, e0 = 0, e1 = 0;
-        uint32_t n0 = 0, n1 = 0, it;
+        uint32_t n0 = 0, n1 = 0;
         bool ok, act0 = false, act1 = false;
         uint64_t d_early;
         if (src.build(k, a, b, e0, n0)) {
-            if (reg_start<W>(a, b, e0, n0, s0, &ok, &it, &d_early)) {
-                its += halve ? (it + 1) >> 1 : it;
+            if (slot_init<W>(a, b, e0, n0, s0, &ok, &d_early)) {
                 fails |= ok ? 0u : 1u << k;
-                src.done(k, ok, d_early, halve ? (it + 1) >> 1 : it);
+                src.done(k, ok, d_early, 0);
             } else {
                 act0 = true;
             }
         }
         if (src.build(k + 1, a, b, e1, n1)) {
-            if (reg_start<W>(a, b, e1, n1, s1, &ok, &it, &d_early)) {
-                its += halve ? (it + 1) >> 1 : it;
+            if (slot_init<W>(a, b, e1, n1, s1, &ok, &d_early)) {
                 fails |= ok ? 0u : 2u << k;
-                src.done(k + 1, ok, d_early, halve ? (it + 1) >> 1 : it);
+                src.done(k + 1, ok, d_early, 0);
             } else {
                 act1 = true;
             }
@@ -301,6 +238,22 @@ __device__ __forceinline__ uint32_t lane_items(Src& src, unsigned long long* ite
         if (!act1) {
             s1 = s0;
             n1 = n0;
+        }
+        {  // iteration 1: the then-half against one (see slot_init)
+            bool f0, f1;
+            pair_step<true, true>(s0, s1, n0, n1, act0, act1, f0, f1);
+            if (act0 && f0) {
+                its += 1;
+                fails |= (s0.d > e0) ? 0u : 1u << k;
+                src.done(k, s0.d > e0, s0.d, 1);
+                act0 = false;
+            }
+            if (act1 && f1) {
+                its += 1;
+                fails |= (s1.d > e1) ? 0u : 2u << k;
+                src.done(k + 1, s1.d > e1, s1.d, 1);
+                act1 = false;
+            }
         }
         uint32_t h = 1;  // half-steps so far (both slots start after their first then-half)
         while (__any_sync(0xffffffffu, act0 || act1)) {
