@@ -1382,34 +1382,48 @@ int hrb_phase3(const hrb_slice* s, int split, const uint64_t* sub_keys, const ui
                        cap, st);
 }
 
+}  // extern "C"
+
+namespace {
+// phases 1-3 of a slice on `st`; ev_p1 (may be null) is recorded once the
+// phase-1 ids and count are final, so a caller can start copying them out
+// while phases 2 and 3 run.  Caller holds g_ws_mu.
+int run_slice_locked(Workspace& ws, const hrb_slice* s, int algo, int mode, int split, const hrb_run_out* out,
+                     cudaStream_t st, cudaEvent_t ev_p1) {
+    int rc;
+    SliceDev sd = to_dev(s);
+    uint64_t* counts = out->counts;
+    CK(cudaMemsetAsync(counts, 0, sizeof(uint64_t) * 4, st));
+    if ((rc = ws_prep(ws, sd, split, st))) return rc;
+    if ((rc = phase1_impl(ws, s, sd, algo, mode, out->fail_ids, counts + 0, out->fail_cap, counts + 3, st)))
+        return rc;
+    if (ev_p1) CK(cudaEventRecord(ev_p1, st));
+    if ((rc = phase2_impl(ws, s, sd, algo, mode, split, out->fail_ids, (const uint32_t*)ws.fail_t.p, counts + 0,
+                          out->fail_cap, out->sub_keys, counts + 1, out->sub_cap, st)))
+        return rc;
+    return phase3_impl(ws, s, sd, split, out->sub_keys, (const uint32_t*)ws.sub_t.p, counts + 1, out->sub_cap,
+                       out->cand_index, out->cand_dist, out->cand_dom, counts + 2, out->cand_cap, st);
+}
+}  // namespace
+
+extern "C" {
+
 int hrb_run_slice(const hrb_slice* s, int algo, int mode, int split, const hrb_run_out* out, void* stream) {
     int rc = check_slice(s);
     if (rc || (rc = check_algo(algo, mode))) return rc;
     if (split < 2 || split > 64) return set_err(HRB_ERR_CONFIG, "phase2_split outside {2..64}");
-    cudaStream_t st = (cudaStream_t)stream;
     std::lock_guard<std::mutex> lk(g_ws_mu);
     Workspace* ws;
     if ((rc = current_ws(&ws))) return rc;
-    SliceDev sd = to_dev(s);
-    uint64_t* counts = out->counts;
-    CK(cudaMemsetAsync(counts, 0, sizeof(uint64_t) * 4, st));
-    if ((rc = ws_prep(*ws, sd, split, st))) return rc;
-    if ((rc = phase1_impl(*ws, s, sd, algo, mode, out->fail_ids, counts + 0, out->fail_cap, counts + 3, st)))
-        return rc;
-    if ((rc = phase2_impl(*ws, s, sd, algo, mode, split, out->fail_ids, (const uint32_t*)ws->fail_t.p, counts + 0,
-                          out->fail_cap, out->sub_keys,
-                          counts + 1, out->sub_cap, st)))
-        return rc;
-    return phase3_impl(*ws, s, sd, split, out->sub_keys, (const uint32_t*)ws->sub_t.p, counts + 1, out->sub_cap,
-                       out->cand_index, out->cand_dist,
-                       out->cand_dom, counts + 2, out->cand_cap, st);
+    return run_slice_locked(*ws, s, algo, mode, split, out, (cudaStream_t)stream, nullptr);
 }
 
 namespace {
 struct HostRunState {
     Buf coef, G, s2, nd, dn, ln, db, m0, fail, sub, cm, cd, cdom, counts;
-    cudaStream_t st = nullptr;
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    cudaStream_t st = nullptr, cs = nullptr;  // compute stream, copy-out stream
+    cudaEvent_t e0 = nullptr, e1 = nullptr, ep1 = nullptr;
+    uint64_t* hcount = nullptr;  // pinned scratch for the phase-1 count
 };
 HostRunState g_host[64];
 }  // namespace
@@ -1424,8 +1438,11 @@ int hrb_run_slice_host(const hrb_slice* hs, int algo, int mode, int split, uint6
     HostRunState& H = g_host[dev & 63];
     if (!H.st) {
         CK(cudaStreamCreateWithFlags(&H.st, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&H.cs, cudaStreamNonBlocking));
         CK(cudaEventCreate(&H.e0));
         CK(cudaEventCreate(&H.e1));
+        CK(cudaEventCreateWithFlags(&H.ep1, cudaEventDisableTiming));
+        CK(cudaMallocHost((void**)&H.hcount, sizeof(uint64_t)));
     }
     const int64_t S = hs->n_super, CL = hs->coef_limbs, NT = hs->n_total;
     const size_t b_coef = sizeof(uint32_t) * 6 * CL * S, b2 = sizeof(uint64_t) * 2 * S, b32 = sizeof(uint32_t) * S;
@@ -1454,6 +1471,7 @@ int hrb_run_slice_host(const hrb_slice* hs, int algo, int mode, int split, uint6
     ds.m0 = (const uint64_t*)H.m0.p;
     uint64_t sub_cap = (uint64_t)NT / 8 + 1024;  // grown once from the true count
     const uint64_t fcap = (uint64_t)NT;
+    bool fail_copied = false;
     for (int attempt = 0; attempt < 2; attempt++) {
         if ((rc = H.fail.ensure(sizeof(uint64_t) * (fcap + 1))) || (rc = H.sub.ensure(sizeof(uint64_t) * (sub_cap + 1))) ||
             (rc = H.cm.ensure(sizeof(uint64_t) * (cand_cap + 1))) ||
@@ -1470,21 +1488,39 @@ int hrb_run_slice_host(const hrb_slice* hs, int algo, int mode, int split, uint6
         o.cand_dom = (uint64_t*)H.cdom.p;
         o.cand_cap = cand_cap;
         o.counts = (uint64_t*)H.counts.p;
-        if ((rc = hrb_run_slice(&ds, algo, mode, split, &o, st))) return rc;
+        {
+            std::lock_guard<std::mutex> lk(g_ws_mu);
+            Workspace* ws;
+            if ((rc = current_ws(&ws))) return rc;
+            if ((rc = check_slice(&ds)) || (rc = check_algo(algo, mode))) return rc;
+            if (split < 2 || split > 64) return set_err(HRB_ERR_CONFIG, "phase2_split outside {2..64}");
+            if ((rc = run_slice_locked(*ws, &ds, algo, mode, split, &o, st, fail_copied ? nullptr : H.ep1))) return rc;
+        }
+        if (!fail_copied) {
+            // the failing ids are final after phase 1: copy them out on the
+            // copy stream while phases 2 and 3 run on the compute stream
+            CK(cudaStreamWaitEvent(H.cs, H.ep1, 0));
+            CK(cudaMemcpyAsync(H.hcount, H.counts.p, sizeof(uint64_t), cudaMemcpyDeviceToHost, H.cs));
+            CK(cudaStreamSynchronize(H.cs));
+            const uint64_t nf0 = *H.hcount < fail_cap ? *H.hcount : fail_cap;
+            if (fail_ids && nf0)
+                CK(cudaMemcpyAsync(fail_ids, H.fail.p, sizeof(uint64_t) * nf0, cudaMemcpyDeviceToHost, H.cs));
+            fail_copied = true;
+        }
         CK(cudaMemcpyAsync(counts, H.counts.p, sizeof(uint64_t) * 4, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         if (counts[1] <= sub_cap) break;
         sub_cap = counts[1] + 1024;  // grow once and re-run
+        CK(cudaStreamSynchronize(H.cs));  // the copy-out of the ids is done before phase 1 rewrites them
         CK(cudaEventRecord(H.e0, st));
     }
-    const uint64_t nf = counts[0] < fail_cap ? counts[0] : fail_cap;
     const uint64_t nc = counts[2] < cand_cap ? counts[2] : cand_cap;
-    if (fail_ids && nf) CK(cudaMemcpyAsync(fail_ids, H.fail.p, sizeof(uint64_t) * nf, cudaMemcpyDeviceToHost, st));
     if (nc) {
         CK(cudaMemcpyAsync(cand_index, H.cm.p, sizeof(uint64_t) * nc, cudaMemcpyDeviceToHost, st));
         CK(cudaMemcpyAsync(cand_dist, H.cd.p, sizeof(uint64_t) * nc, cudaMemcpyDeviceToHost, st));
         CK(cudaMemcpyAsync(cand_dom, H.cdom.p, sizeof(uint64_t) * nc, cudaMemcpyDeviceToHost, st));
     }
+    CK(cudaStreamSynchronize(H.cs));
     CK(cudaEventRecord(H.e1, st));
     CK(cudaStreamSynchronize(st));
     if (device_ms) CK(cudaEventElapsedTime(device_ms, H.e0, H.e1));

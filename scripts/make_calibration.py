@@ -16,11 +16,26 @@ SOURCES = ["paper_1211_3056_b200/csrc/hrb200.cu", "paper_1211_3056_b200/csrc/til
            "paper_1211_3056_b200/csrc/search_core.cuh"]
 
 
+def _kernel_text(path: str, name: str) -> bytes:
+    """The source text of one __global__ function (signature to closing brace)."""
+    text = open(os.path.join(ROOT, path)).read()
+    i = text.index(name + "(")
+    i = text.rfind("\n", 0, text.rfind("__global__", 0, i)) + 1
+    j = text.index("\n}\n", i) + 3
+    return text[i:j].encode()
+
+
 def source_sha() -> str:
+    """Hash of what the phase-1 instruction count depends on: the search
+    headers, the phase-1 kernel and its walk source (host code excluded)."""
     h = hashlib.sha256()
-    for p in SOURCES:
+    for p in SOURCES[1:]:
         with open(os.path.join(ROOT, p), "rb") as fh:
             h.update(fh.read())
+    h.update(_kernel_text(SOURCES[0], "phase1_reg_kernel"))
+    text = open(os.path.join(ROOT, SOURCES[0])).read()
+    i = text.index("struct WalkSrc")
+    h.update(text[i:text.index("\n};\n", i)].encode())
     return h.hexdigest()[:16]
 
 
