@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(256) phase1_kernel(SliceDev s, int algo, int m
     const u128 mF = mask_f(s.F);
     unsigned long long iters = 0;
     for (uint64_t gw = warp0; gw < total_tiles; gw += nwarps) {
-        const int64_t t = find_seg(tile_base, s.S, gw);
+        const int64_t t = locate_super(tile_base, s.S, gw);
         const uint64_t tile = gw - tile_base[t];
         const uint32_t nd = __ldg(&s.n_dom[t]);
         const u128 c00 = coef_res(s, t, 0), c01 = coef_res(s, t, 1), c02 = coef_res(s, t, 2);
@@ -345,7 +345,7 @@ __global__ void __launch_bounds__(128, HRB_P1_MINB) phase1_reg_kernel(SliceDev s
     src.inc = incs[threadIdx.x >> 5];
     src.sh = 128 - s.F;
     for (uint64_t gw = warp0; gw < total_tiles; gw += nwarps) {
-        const int64_t t = find_seg(tile_base, s.S, gw);
+        const int64_t t = locate_super(tile_base, s.S, gw);
         const uint64_t tile = gw - tile_base[t];
         const u128 c00 = coef_res(s, t, 0), c01 = coef_res(s, t, 1), c02 = coef_res(s, t, 2);
         const u128 c10 = coef_res(s, t, 3), c11 = coef_res(s, t, 4);
@@ -877,7 +877,7 @@ __global__ void __launch_bounds__(128) tabdiff_full_kernel(SliceDev s, const uin
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const uint64_t total_tiles = tile_base[s.S];
     for (uint64_t gw = warp0; gw < total_tiles; gw += nwarps) {
-        const int64_t t = find_seg(tile_base, s.S, gw);
+        const int64_t t = locate_super(tile_base, s.S, gw);
         const uint64_t tile = gw - tile_base[t];
         const uint32_t nd = __ldg(&s.n_dom[t]);
         const uint64_t il = tile * TILE + lane;

@@ -69,24 +69,34 @@ constexpr int32_t QMAX = 1 << 20;
 // estimate is clamped at 0 and a wrapped subtraction is caught directly
 // (result above its minuend), since ">= S" no longer implies a wrap there.
 template <bool THEN, bool FIRST = false>
-__device__ __forceinline__ void hs_fast(uint64_t L, uint64_t S, float Lf, float Sf, uint64_t d, uint64_t& Lp,
-                                        uint64_t& dn, uint32_t& k, bool& bad) {
+__device__ __forceinline__ void hs_fast(uint64_t& L, uint64_t S, float Lf, float Sf, uint64_t& d, uint32_t& k,
+                                        uint32_t& k2, bool& sub, bool& bad) {
     const float rcp = rcp_approx(Sf);
     // floor(L/S) >= 1 except on a first step, so the estimate is >= 0
     const int32_t ke = FIRST ? max(qfloor(Lf, rcp), 0) : qfloor(Lf, rcp);
     const uint64_t r = L - (uint64_t)(uint32_t)ke * S;
     uint64_t x = d;
-    if (!THEN && x >= r) x -= r;
+    sub = !THEN && x >= r;
+    if (sub) x -= r;
     // the quotient of x by S is >= 0; an estimate of -1 (x/S within |e| of
     // 0 from above) is clamped to 0, which is then exact
     const uint32_t ke2 = (uint32_t)max(qfloor(__ull2float_rn(x), rcp), 0);
     const uint64_t y = x - (uint64_t)ke2 * S;
     bad = (ke >= QMAX) | (r >= S) | (y >= S);
     if (FIRST) bad |= (r > L) | (y > x);
-    Lp = r;
-    dn = y;
+    // in place: the old L and d are recoverable from (r, y, ke, ke2, sub)
+    // on the exact path, so no copy of them stays live across the vote
+    L = r;
+    d = y;
     k = (uint32_t)ke;
+    k2 = ke2;
 }
+
+// Undo hs_fast's in-place update (all arithmetic mod 2^64 is exact) and
+// redo the half-step with hardware division.
+__device__ __forceinline__ void hs_redo(uint64_t& L, uint64_t S, uint64_t& d, uint32_t& k, uint32_t k2, bool sub,
+                                        bool then_body);
+
 
 // The same half-step with hardware 64-bit division (rare: a quotient >= 2^20
 // or an estimate that missed by one).
@@ -108,18 +118,26 @@ __device__ __noinline__ ExactStep hs_exact(uint64_t L, uint64_t S, uint64_t d, b
     return e;
 }
 
-// Commit a half-step in place (L <- Lp, cL <- k cS + cL, d <- dn) and report
-// whether the search ended: expansion exhausted (Lp == 0) or the count
-// reaches N.  A finished slot keeps computing harmless garbage.
-__device__ __forceinline__ bool hs_commit(uint64_t& L, float& Lf, uint32_t& cL, uint32_t cS, uint64_t& d, uint32_t N,
-                                          uint64_t Lp, uint64_t dn, uint32_t k) {
+// Finish a half-step (L and d already updated in place): cL <- k cS + cL and
+// the float copy of L, and report whether the search ended: expansion
+// exhausted (L == 0) or the count reaches N.  A finished slot keeps
+// computing harmless garbage.
+__device__ __forceinline__ bool hs_commit(uint64_t L, float& Lf, uint32_t& cL, uint32_t cS, uint32_t N, uint32_t k) {
     const uint64_t cLp = (uint64_t)k * cS + cL;
-    const bool done = Lp == 0 || cLp >= (uint64_t)(N - cS);
-    L = Lp;
-    Lf = __ull2float_rn(Lp);
+    const bool done = L == 0 || cLp >= (uint64_t)(N - cS);
+    Lf = __ull2float_rn(L);
     cL = (uint32_t)cLp;
-    d = dn;
     return done;
+}
+
+__device__ __forceinline__ void hs_redo(uint64_t& L, uint64_t S, uint64_t& d, uint32_t& k, uint32_t k2, bool sub,
+                                        bool then_body) {
+    const uint64_t L_old = L + (uint64_t)k * S;
+    const uint64_t d_old = d + (uint64_t)k2 * S + (sub ? L : 0);
+    const ExactStep e = hs_exact(L_old, S, d_old, then_body);
+    L = e.Lp;
+    d = e.dn;
+    k = e.k;
 }
 
 // Both slots of a lane advance one half-step: the else-half divides B by A,
@@ -140,25 +158,73 @@ __device__ __forceinline__ void pair_step(Slot& s0, Slot& s1, uint32_t n0, uint3
     uint32_t& cL0 = THEN ? s0.cA : s0.cB;
     uint32_t& cL1 = THEN ? s1.cA : s1.cB;
     const uint32_t cS0 = THEN ? s0.cB : s0.cA, cS1 = THEN ? s1.cB : s1.cA;
-    uint64_t Lp0, dn0, Lp1, dn1;
-    uint32_t k0, k1;
-    bool b0, b1;
-    hs_fast<THEN, FIRST>(L0, S0, Lf0, Sf0, s0.d, Lp0, dn0, k0, b0);
-    hs_fast<THEN, FIRST>(L1, S1, Lf1, Sf1, s1.d, Lp1, dn1, k1, b1);
+    uint32_t k0, k1, q0, q1;
+    bool b0, b1, u0, u1;
+    hs_fast<THEN, FIRST>(L0, S0, Lf0, Sf0, s0.d, k0, q0, u0, b0);
+    hs_fast<THEN, FIRST>(L1, S1, Lf1, Sf1, s1.d, k1, q1, u1, b1);
     b0 = b0 && act0;
     b1 = b1 && act1;
     if (__any_sync(0xffffffffu, b0 || b1)) {
-        if (b0) {
-            const ExactStep e = hs_exact(L0, S0, s0.d, THEN);
-            Lp0 = e.Lp, dn0 = e.dn, k0 = e.k;
-        }
-        if (b1) {
-            const ExactStep e = hs_exact(L1, S1, s1.d, THEN);
-            Lp1 = e.Lp, dn1 = e.dn, k1 = e.k;
-        }
+        if (b0) hs_redo(L0, S0, s0.d, k0, q0, u0, THEN);
+        if (b1) hs_redo(L1, S1, s1.d, k1, q1, u1, THEN);
     }
-    f0 = hs_commit(L0, Lf0, cL0, cS0, s0.d, n0, Lp0, dn0, k0);
-    f1 = hs_commit(L1, Lf1, cL1, cS1, s1.d, n1, Lp1, dn1, k1);
+    f0 = hs_commit(L0, Lf0, cL0, cS0, n0, k0);
+    f1 = hs_commit(L1, Lf1, cL1, cS1, n1, k1);
+}
+
+// The lockstep loop's two building blocks.  fast_pair advances both slots
+// by one half-step in place and votes: it returns true when some active
+// lane's estimate may be wrong, in which case the caller leaves the loop
+// (no commit) and finishes the pair on the exact path -- keeping every
+// repair out of the loop body, whose registers then never merge with it.
+template <bool THEN>
+__device__ __forceinline__ bool fast_pair(Slot& s0, Slot& s1, bool act0, bool act1, uint32_t& k0, uint32_t& k1,
+                                          uint32_t& q0, uint32_t& q1, bool& u0, bool& u1, bool& b0, bool& b1) {
+    uint64_t& L0 = THEN ? s0.A : s0.B;
+    uint64_t& L1 = THEN ? s1.A : s1.B;
+    hs_fast<THEN>(L0, THEN ? s0.B : s0.A, THEN ? s0.Af : s0.Bf, THEN ? s0.Bf : s0.Af, s0.d, k0, q0, u0, b0);
+    hs_fast<THEN>(L1, THEN ? s1.B : s1.A, THEN ? s1.Af : s1.Bf, THEN ? s1.Bf : s1.Af, s1.d, k1, q1, u1, b1);
+    b0 = b0 && act0;
+    b1 = b1 && act1;
+    return __any_sync(0xffffffffu, b0 || b1);
+}
+
+template <bool THEN>
+__device__ __forceinline__ bool commit_slot(Slot& s, uint32_t n, uint32_t k) {
+    return THEN ? hs_commit(s.A, s.Af, s.cA, s.cB, n, k) : hs_commit(s.B, s.Bf, s.cB, s.cA, n, k);
+}
+
+// One exact half-step of parity `th` from a slot's committed state.
+__device__ __forceinline__ bool exact_half(Slot& s, bool th, uint32_t n) {
+    if (th) {
+        const ExactStep e = hs_exact(s.A, s.B, s.d, true);
+        s.A = e.Lp;
+        s.d = e.dn;
+        return hs_commit(s.A, s.Af, s.cA, s.cB, n, e.k);
+    }
+    const ExactStep e = hs_exact(s.B, s.A, s.d, false);
+    s.B = e.Lp;
+    s.d = e.dn;
+    return hs_commit(s.B, s.Bf, s.cB, s.cA, n, e.k);
+}
+
+// Rare path: repair the half-step of parity `th` that fast_pair left
+// uncommitted (redo it exactly where it was flagged), commit it, then run
+// the slot's search to its end with exact half-steps.  Returns the
+// half-step count at the end.
+__device__ __noinline__ uint32_t slow_finish(Slot& s, bool bad, uint32_t k, uint32_t q, bool u, bool th, uint32_t h,
+                                             uint32_t n) {
+    uint64_t& L = th ? s.A : s.B;
+    const uint64_t S = th ? s.B : s.A;
+    if (bad) hs_redo(L, S, s.d, k, q, u, th);
+    bool f = th ? hs_commit(s.A, s.Af, s.cA, s.cB, n, k) : hs_commit(s.B, s.Bf, s.cB, s.cA, n, k);
+    h++;
+    while (!f) {
+        th = !th;
+        f = exact_half(s, th, n);
+        h++;
+    }
+    return h;
 }
 
 // Set up a slot for _regular_core (lowerbound.py:228-267).  Returns true if
@@ -208,9 +274,9 @@ __device__ __forceinline__ uint32_t lane_items(Src& src, unsigned long long* ite
     uint32_t fails = 0, its = 0;
     const uint32_t mine = n_items < (uint32_t)NU ? n_items : (uint32_t)NU;
     const int kend = (int)__reduce_max_sync(0xffffffffu, mine);
+    Slot s0 = {}, s1 = {};
 #pragma unroll 1
     for (int k = 0; k < kend; k += 2) {
-        Slot s0, s1;
         uint64_t a, b, e0 = 0, e1 = 0;
         uint32_t n0 = 0, n1 = 0;
         bool ok, act0 = false, act1 = false;
@@ -231,14 +297,9 @@ __device__ __forceinline__ uint32_t lane_items(Src& src, unsigned long long* ite
                 act1 = true;
             }
         }
-        if (!act0) {  // keep the idle chain's arithmetic well defined
-            s0 = s1;
-            n0 = n1;
-        }
-        if (!act1) {
-            s1 = s0;
-            n1 = n0;
-        }
+        // An idle slot keeps whatever state it holds: its arithmetic may be
+        // garbage (integer ops do not trap, and an idle slot's `bad` flag is
+        // masked), so nothing is copied into it.
         {  // iteration 1: the then-half against one (see slot_init)
             bool f0, f1;
             pair_step<true, true>(s0, s1, n0, n1, act0, act1, f0, f1);
@@ -256,9 +317,15 @@ __device__ __forceinline__ uint32_t lane_items(Src& src, unsigned long long* ite
             }
         }
         uint32_t h = 1;  // half-steps so far (both slots start after their first then-half)
+        int pending = 0;  // 1 / 2: left the loop with an uncommitted else- / then-half
+        uint32_t k0, k1, q0, q1;
+        bool u0, u1, b0, b1;
         while (__any_sync(0xffffffffu, act0 || act1)) {
-            bool f0, f1;
-            pair_step<false>(s0, s1, n0, n1, act0, act1, f0, f1);
+            if (fast_pair<false>(s0, s1, act0, act1, k0, k1, q0, q1, u0, u1, b0, b1)) {
+                pending = 1;
+                break;
+            }
+            bool f0 = commit_slot<false>(s0, n0, k0), f1 = commit_slot<false>(s1, n1, k1);
             h++;
             if (act0 && f0) {
                 its += halve ? (h + 1) >> 1 : h;
@@ -272,7 +339,11 @@ __device__ __forceinline__ uint32_t lane_items(Src& src, unsigned long long* ite
                 src.done(k + 1, s1.d > e1, s1.d, halve ? (h + 1) >> 1 : h);
                 act1 = false;
             }
-            pair_step<true>(s0, s1, n0, n1, act0, act1, f0, f1);
+            if (fast_pair<true>(s0, s1, act0, act1, k0, k1, q0, q1, u0, u1, b0, b1)) {
+                pending = 2;
+                break;
+            }
+            f0 = commit_slot<true>(s0, n0, k0), f1 = commit_slot<true>(s1, n1, k1);
             h++;
             if (act0 && f0) {
                 its += halve ? (h + 1) >> 1 : h;
@@ -285,6 +356,21 @@ __device__ __forceinline__ uint32_t lane_items(Src& src, unsigned long long* ite
                 fails |= (s1.d > e1) ? 0u : 2u << k;
                 src.done(k + 1, s1.d > e1, s1.d, halve ? (h + 1) >> 1 : h);
                 act1 = false;
+            }
+        }
+        if (pending) {  // rare (warp-uniform entry): finish the pair's searches exactly
+            const bool th = pending == 2;
+            if (act0) {
+                const uint32_t hh = slow_finish(s0, b0, k0, q0, u0, th, h, n0);
+                its += halve ? (hh + 1) >> 1 : hh;
+                fails |= (s0.d > e0) ? 0u : 1u << k;
+                src.done(k, s0.d > e0, s0.d, halve ? (hh + 1) >> 1 : hh);
+            }
+            if (act1) {
+                const uint32_t hh = slow_finish(s1, b1, k1, q1, u1, th, h, n1);
+                its += halve ? (hh + 1) >> 1 : hh;
+                fails |= (s1.d > e1) ? 0u : 2u << k;
+                src.done(k + 1, s1.d > e1, s1.d, halve ? (hh + 1) >> 1 : hh);
             }
         }
     }
