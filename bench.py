@@ -206,6 +206,22 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def hbm_side(traffic, kernel_ms):
+    """The memory side of the same kernel: ncu DRAM bytes per launch over the
+    live launch time, against the measured HBM copy peak (MEASURED_PEAKS.json)
+    -- shows the path is nowhere near memory bound."""
+    if not traffic:
+        return None
+    peak = None
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            peak = json.load(fh).get("hbm_gbs")
+    gbs = traffic / (kernel_ms / 1e3) / 1e9
+    return {"achieved_gbs": gbs, "peak_gbs": peak, "frac": gbs / peak if peak else None,
+            "peak_basis": "measured (MEASURED_PEAKS.json hbm_gbs)" if peak else None}
+
+
 def int_peak():
     """Measured INT-pipe issue peak (lane-ops/s) of this device: IADD3 + IMAD
     chains, and IADD3 alone (csrc/intpeak.cu)."""
@@ -374,6 +390,7 @@ def main():
                 if achieved else None,
                 "peak_probes": {k: v / 1e12 for k, v in peak.items()},
                 "traffic": k1.get("dram_bytes_per_launch"),
+                "hbm": hbm_side(k1.get("dram_bytes_per_launch"), p1_max),
                 "algorithmic_unit": "CF quotient step (SearchOutcome.iterations)",
                 "quotient_steps_per_launch": iters, "kernel_ms": p1_max,
                 "quotient_steps_per_s": iters / (p1_max / 1e3),
