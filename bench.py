@@ -35,8 +35,8 @@ sys.path.insert(0, ROOT)
 
 METRIC = "binary64 args tested/sec (exp) at 1/2/4/8 B200 vs CPU ref; % of INT-pipe peak"
 UNIT = "args/s"
-# kernels per hrb_run_slice: prep, cub scan (2), phase1 + 3 compaction, phase2 + 3, phase3 + 3 + scatter
-KERNELS_PER_STEP = 16
+# kernels per hrb_run_slice: prep, cub scan (2), phase1 + 3 compaction, phase2 + 3, chunk choice, phase3 + 3 + scatter
+KERNELS_PER_STEP = 17
 CALIBRATION = os.path.join(ROOT, "profiles", "calibration.json")
 
 

@@ -14,11 +14,9 @@
 //   * 65-bit point totals, returned as (lo, hi).
 //
 // Division: quotients are Gauss-Kuzmin distributed (mostly 1..3), so a
-// quotient is estimated in FP64 from a Newton-refined reciprocal of the
-// divisor (one reciprocal per divisor, shared by the two divisions of a
-// regular half-step) and fixed with one compare; quotients >= 2^32 take the
-// exact hardware path.  The FP64 work issues on the FP64 pipe, beside the
-// integer pipes that carry the rest of the step.
+// quotient is estimated from an FP32 reciprocal of the divisor (one per
+// divisor, shared by the two divisions of a regular half-step) and fixed with
+// one compare; quotients >= 2^20 take the exact hardware path.
 #pragma once
 #include <stdint.h>
 
@@ -64,35 +62,37 @@ struct BitTrace {  // decisions as bits, LSB first; len counts every decision
     }
 };
 
-// ~1/x to ~2^-44 relative: MUFU.RCP64H seed + one Newton step.
-__device__ __forceinline__ double recip_est(uint64_t x) {
-    double xd = __ull2double_rn(x);
-    double r;
-    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(xd));
-    double e = fma(-xd, r, 1.0);
-    return fma(r, e, r);
+// FP32 reciprocal of x (<= 1 ulp; MUFU.RCP), shared by the divisions of a step.
+__device__ __forceinline__ float recip_f32(uint64_t x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(__ull2float_rn(x)));
+    return r;
 }
 
-// k = floor(y / x), r = y - k x, given xinv ~ 1/x.  The estimate
-// kd = y*xinv - 1/2 lies in (y/x - 1, y/x) whenever y/x < 2^32, so its
-// truncation is k or k-1 and one compare finishes it.
-__device__ __forceinline__ uint64_t divmod_est(uint64_t y, uint64_t x, double xinv, uint64_t& r) {
-    double kd = fma(__ull2double_rn(y), xinv, -0.5);
-    if (kd < 4294967296.0) {
-        uint32_t k = __double2uint_rz(kd);  // saturates negatives to 0
-        uint64_t rr = y - (uint64_t)k * x;
-        bool c = rr >= x;
+// k = floor(y / x), r = y - k x, given rcp ~ 1/x.  With M = 1.5 * 2^23 the
+// FFMA y*rcp + (M - 1) lands on the integer grid of [2^23, 2^24), so its
+// single rounding is round(y/x - 1 + e) with |e| < 2^-21 y/x: for y/x < 2^20
+// that is floor(y/x) or floor(y/x) - 1 (-1 clamped to 0, where y < x), read
+// from the bit pattern; one compare finishes it.  Larger quotients (and
+// estimates off the grid) take the hardware division.
+__device__ __forceinline__ uint64_t divmod_est(uint64_t y, uint64_t x, float rcp, uint64_t& r) {
+    const float kf = fmaf(__ull2float_rn(y), rcp, 12582911.0f);
+    const int32_t ke = (int32_t)(__float_as_uint(kf) - 0x4B400000u);
+    if (ke < (1 << 20)) {
+        const uint32_t k = (uint32_t)max(ke, 0);
+        const uint64_t rr = y - (uint64_t)k * x;
+        const bool c = rr >= x;
         r = c ? rr - x : rr;
         return (uint64_t)k + (c ? 1u : 0u);
     }
-    uint64_t k = y / x;
+    const uint64_t k = y / x;
     r = y - k * x;
     return k;
 }
 
-__device__ __forceinline__ uint64_t mod_est(uint64_t y, uint64_t x, double xinv) {
+__device__ __forceinline__ uint64_t mod_est(uint64_t y, uint64_t x, float rcp) {
     uint64_t r;
-    divmod_est(y, x, xinv, r);
+    divmod_est(y, x, rcp, r);
     return r;
 }
 
@@ -184,7 +184,7 @@ __device__ __forceinline__ bool reg_begin(uint64_t a, uint64_t b, uint64_t eps, 
 template <int W, class Tr = NoTrace>
 __device__ __forceinline__ bool reg_step(RegState& st, Outcome* out, Tr* tr = nullptr, bool unrolled = false) {
     const uint64_t S = st.S;
-    double sinv = recip_est(S);
+    const float sinv = recip_f32(S);
     uint64_t Lp;
     uint64_t k = divmod_est(st.L, S, sinv, Lp);
     uint64_t cLp = st.cL + k * st.cS;  // exact unless exhausted with S == 1 (see below)
@@ -324,7 +324,7 @@ __device__ __forceinline__ bool lef_step(LefState& st, int mode, Outcome* out, T
     uint64_t k = 0;
     if (st.q >= st.p) {
         uint64_t r;
-        k = divmod_est(st.q, st.p, recip_est(st.p), r);
+        k = divmod_est(st.q, st.p, recip_f32(st.p), r);
     }
     uint64_t s = st.u + st.v;
     bool c = s < st.u;
