@@ -24,9 +24,12 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <atomic>
 #include <cub/cub.cuh>
+#include <cstdlib>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/hrb200.h"
 #include "search_core.cuh"
@@ -1033,6 +1036,10 @@ __global__ void __launch_bounds__(256) search_trace_kernel(int algo, int mode, i
 // ---------------------------------------------------------------------------
 // workspace (per device, grows; guarded by a mutex)
 // ---------------------------------------------------------------------------
+// bumped on every device (re)allocation: a captured graph is only replayed
+// while the workspace pointers it baked in are still the live ones
+std::atomic<uint64_t> g_alloc_gen{0};
+
 struct Buf {
     void* p = nullptr;
     size_t n = 0;
@@ -1044,6 +1051,7 @@ struct Buf {
         size_t want = bytes + bytes / 4 + 256;
         CK(cudaMalloc(&p, want));
         n = want;
+        g_alloc_gen++;
         return HRB_OK;
     }
 };
@@ -1404,6 +1412,58 @@ int run_slice_locked(Workspace& ws, const hrb_slice* s, int algo, int mode, int 
     return phase3_impl(ws, s, sd, split, out->sub_keys, (const uint32_t*)ws.sub_t.p, counts + 1, out->sub_cap,
                        out->cand_index, out->cand_dist, out->cand_dom, counts + 2, out->cand_cap, st);
 }
+
+// hrb_run_slice replays its 17 launches as one CUDA graph when called again
+// with identical arguments (the bench and every re-run of a resident slice):
+// the first call runs eagerly -- sizing the workspace -- and captures the same
+// sequence on a private stream; later identical calls launch the graph on the
+// caller's stream.  HRB_NO_GRAPH=1 disables it.
+struct GraphCache {
+    bool valid = false;
+    std::vector<uint64_t> key;
+    uint64_t gen = 0;
+    cudaGraphExec_t exec = nullptr;
+    cudaStream_t cap = nullptr;
+};
+GraphCache g_graph[64];
+
+std::vector<uint64_t> run_key(const hrb_slice* s, int algo, int mode, int split, const hrb_run_out* o) {
+    return {(uint64_t)s->n_super, (uint64_t)s->n_total, s->max_dom_n, (uint64_t)s->coef_limbs, (uint64_t)s->frac_bits,
+            (uint64_t)s->word_bits, (uint64_t)s->delta, (uint64_t)s->coef, (uint64_t)s->G, (uint64_t)s->s2abs,
+            (uint64_t)s->n_dom, (uint64_t)s->dom_n, (uint64_t)s->last_n, (uint64_t)s->dom_base, (uint64_t)s->m0,
+            (uint64_t)algo, (uint64_t)mode, (uint64_t)split, (uint64_t)o->fail_ids, o->fail_cap, (uint64_t)o->sub_keys,
+            o->sub_cap, (uint64_t)o->cand_index, (uint64_t)o->cand_dist, (uint64_t)o->cand_dom, o->cand_cap,
+            (uint64_t)o->counts};
+}
+
+int capture_run(GraphCache& G, Workspace& ws, const hrb_slice* s, int algo, int mode, int split, const hrb_run_out* out,
+                std::vector<uint64_t>&& key) {
+    if (!G.cap) CK(cudaStreamCreateWithFlags(&G.cap, cudaStreamNonBlocking));
+    const uint64_t gen0 = g_alloc_gen.load();
+    CK(cudaStreamBeginCapture(G.cap, cudaStreamCaptureModeThreadLocal));
+    int rc = run_slice_locked(ws, s, algo, mode, split, out, G.cap, nullptr);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ec = cudaStreamEndCapture(G.cap, &graph);
+    G.valid = false;
+    if (rc || ec != cudaSuccess || !graph || g_alloc_gen.load() != gen0) {
+        if (graph) cudaGraphDestroy(graph);
+        cudaGetLastError();  // a failed capture is not an error of the run itself
+        return HRB_OK;
+    }
+    if (G.exec) cudaGraphExecDestroy(G.exec);
+    G.exec = nullptr;
+    const cudaError_t ei = cudaGraphInstantiate(&G.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ei != cudaSuccess) {
+        G.exec = nullptr;
+        cudaGetLastError();
+        return HRB_OK;
+    }
+    G.key = std::move(key);
+    G.gen = gen0;
+    G.valid = true;
+    return HRB_OK;
+}
 }  // namespace
 
 extern "C" {
@@ -1415,7 +1475,17 @@ int hrb_run_slice(const hrb_slice* s, int algo, int mode, int split, const hrb_r
     std::lock_guard<std::mutex> lk(g_ws_mu);
     Workspace* ws;
     if ((rc = current_ws(&ws))) return rc;
-    return run_slice_locked(*ws, s, algo, mode, split, out, (cudaStream_t)stream, nullptr);
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    GraphCache& G = g_graph[dev & 63];
+    const bool use_graph = std::getenv("HRB_NO_GRAPH") == nullptr;
+    std::vector<uint64_t> key = run_key(s, algo, mode, split, out);
+    if (use_graph && G.valid && G.gen == g_alloc_gen.load() && G.key == key) {
+        CK(cudaGraphLaunch(G.exec, (cudaStream_t)stream));
+        return HRB_OK;
+    }
+    if ((rc = run_slice_locked(*ws, s, algo, mode, split, out, (cudaStream_t)stream, nullptr))) return rc;
+    return use_graph ? capture_run(G, *ws, s, algo, mode, split, out, std::move(key)) : HRB_OK;
 }
 
 namespace {
