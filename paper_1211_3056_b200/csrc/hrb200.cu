@@ -115,15 +115,27 @@ SliceDev to_dev(const hrb_slice* s) {
 
 __device__ __forceinline__ u128 mask_f(int F) { return F >= 128 ? ~(u128)0 : (((u128)1 << F) - 1); }
 
-// residue mod 2^128 of packed coefficient c of super-domain t
+// residue mod 2^128 of packed coefficient c of super-domain t: with at least
+// four two's-complement limbs it is just the low four limbs (the common case,
+// CL = L + 1 = 9; four loads, no shifts); narrower coefficients are
+// sign-extended
 __device__ __forceinline__ u128 coef_res(const SliceDev& s, int64_t t, int c) {
-    u128 r = 0;
-    int lim = s.CL < 4 ? s.CL : 4;
-    for (int l = 0; l < lim; l++) r |= (u128)__ldg(&s.coef[((int64_t)c * s.CL + l) * s.S + t]) << (32 * l);
-    if (s.CL < 4 && (__ldg(&s.coef[((int64_t)c * s.CL + s.CL - 1) * s.S + t]) & 0x80000000u)) {
-        r |= ~(u128)0 << (32 * s.CL);  // sign-extend
+    const uint32_t* base = s.coef + (int64_t)c * s.CL * s.S + t;
+    if (s.CL >= 4) {
+        const uint64_t lo = (uint64_t)__ldg(base) | ((uint64_t)__ldg(base + s.S) << 32);
+        const uint64_t hi = (uint64_t)__ldg(base + 2 * s.S) | ((uint64_t)__ldg(base + 3 * s.S) << 32);
+        return ((u128)hi << 64) | lo;
     }
+    u128 r = 0;
+    for (int l = 0; l < s.CL; l++) r |= (u128)__ldg(base + l * s.S) << (32 * l);
+    if (__ldg(base + (s.CL - 1) * s.S) & 0x80000000u) r |= ~(u128)0 << (32 * s.CL);  // sign-extend
     return r;
+}
+
+// a / b for b < 2^32 through the 32-bit divide when a fits 32 bits (always on
+// the pipeline's domain sizes); the 64-bit divide is a CALL to a long routine
+__device__ __forceinline__ uint64_t udiv_small(uint64_t a, uint32_t b) {
+    return (a >> 32) ? a / b : (uint64_t)((uint32_t)a / b);
 }
 
 __device__ __forceinline__ u128 ld128(const uint64_t* p, int64_t S, int64_t t) {
@@ -436,9 +448,9 @@ __global__ void __launch_bounds__(128, HRB_P2_MINB) phase2_reg_kernel(SliceDev s
             const int64_t t = fail_t[f];
             const uint64_t i = id - __ldg(&s.dom_base[t]);
             const uint64_t n = domain_size(s, t, i);
-            uint64_t step = n / (uint64_t)split;
+            uint64_t step = udiv_small(n, (uint32_t)split);
             if (step < 1) step = 1;
-            const uint64_t nsub = (n + step - 1) / step;
+            const uint64_t nsub = udiv_small(n + step - 1, (uint32_t)step);
             const u128 c00 = coef_res(s, t, 0), c01 = coef_res(s, t, 1), c02 = coef_res(s, t, 2);
             const u128 c10 = coef_res(s, t, 3), c11 = coef_res(s, t, 4);
             const u128 s2 = s.delta >= 2 ? coef_res(s, t, 5) : (u128)0;
@@ -482,9 +494,9 @@ __global__ void __launch_bounds__(256) phase2_classic_kernel(SliceDev s, int mod
         const int64_t t = fail_t[f];
         const uint64_t i = id - __ldg(&s.dom_base[t]);
         const uint64_t n = domain_size(s, t, i);
-        uint64_t step = n / (uint64_t)split;
+        uint64_t step = udiv_small(n, (uint32_t)split);
         if (step < 1) step = 1;
-        const uint64_t nsub = (n + step - 1) / step;
+        const uint64_t nsub = udiv_small(n + step - 1, (uint32_t)step);
         const u128 c00 = coef_res(s, t, 0), c01 = coef_res(s, t, 1), c02 = coef_res(s, t, 2);
         const u128 c10 = coef_res(s, t, 3), c11 = coef_res(s, t, 4);
         const u128 s2 = s.delta >= 2 ? coef_res(s, t, 5) : (u128)0;
@@ -611,14 +623,14 @@ __global__ void __launch_bounds__(256) phase3_kernel(SliceDev s, int split, cons
         uint64_t mbase = 0, dom = 0;
         u128 V = 0, D1 = 0, D2 = 0, K = 0, wm1 = 0;
         if (g < n_items) {
-            const uint64_t r = g / CH, c = g - r * CH;
+            const uint64_t r = udiv_small(g, (uint32_t)CH), c = g - r * CH;
             const uint64_t key = sub_keys[r];
             dom = key >> 8;
             const uint64_t j = key & 255;
             const int64_t t = sub_t[r];
             const uint64_t i = dom - s.dom_base[t];
             const uint64_t n = domain_size(s, t, i);
-            uint64_t step = n / split;
+            uint64_t step = udiv_small(n, (uint32_t)split);
             if (step < 1) step = 1;
             const uint64_t start = j * step;
             const uint64_t cnt = n - start < step ? n - start : step;
