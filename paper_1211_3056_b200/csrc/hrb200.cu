@@ -601,8 +601,11 @@ __global__ void chunk3_kernel(unsigned long long* meta, const uint64_t* sub_coun
 // top 64 bits over 32 arguments; when some lane of the warp flagged, the
 // warp re-walks those 32 arguments exactly and appends the candidates with
 // __ballot_sync/__popc (one atomic per warp).
+#ifndef HRB_P3_MINB
+#define HRB_P3_MINB 3
+#endif
 template <bool NARROW>
-__global__ void __launch_bounds__(256) phase3_kernel(SliceDev s, int split, const uint64_t* sub_keys,
+__global__ void __launch_bounds__(256, HRB_P3_MINB) phase3_kernel(SliceDev s, int split, const uint64_t* sub_keys,
                                                      const uint32_t* sub_t, const uint64_t* sub_count,
                                                      uint64_t sub_cap, const unsigned long long* meta,
                                                      uint32_t* item_counts, Cand* app, unsigned long long* app_count,
