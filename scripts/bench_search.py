@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--log2-N", type=int, default=15)
     ap.add_argument("--reps", type=int, default=50)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--verdicts", action="store_true", help="also time the lockstep form (hrb_search_verdicts)")
     a = ap.parse_args()
     import torch
 
@@ -79,6 +80,26 @@ def main():
             rec["bit_exact_vs_oracle"] = bool(np.array_equal(wit, iters) and np.array_equal(wd, d.cpu().numpy().view(np.uint64))
                                               and np.array_equal(wok, ok.cpu().numpy()))
         out["algos"][name] = rec
+    if a.verdicts:  # the phases' lockstep form of the regular family (verdict, d, iterations only)
+        for name, code in (("regular_lockstep", 2), ("regular_unrolled_lockstep", 3)):
+            def launch_v():
+                nat.check("hrb_search_verdicts", lib.hrb_search_verdicts(code, 64, n, *(x.data_ptr() for x in ins),
+                                                                         ok.data_ptr(), d.data_ptr(), it.data_ptr(),
+                                                                         nat.stream_ptr()))
+            for _ in range(3):
+                launch_v()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(a.reps):
+                launch_v()
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / a.reps
+            iters = it.cpu().numpy().view(np.uint64)
+            out["algos"][name] = {"kernel_ms": ms, "args_per_s": args_total / (ms / 1e3),
+                                  "quotient_steps_per_s": float(iters.sum()) / (ms / 1e3),
+                                  "it_mean": float(iters.mean()), "mean_nmdm": warp_summary(iters).mean_nmdm}
     print(json.dumps(out), flush=True)
 
 

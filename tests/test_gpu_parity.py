@@ -334,3 +334,34 @@ def test_search_verdicts_w32_vs_reference_goldens():
         ok, d, it = search_verdict_arrays(ALGO_CODE[algo], 32, g["a"], g["b"], g["eps"], g["count"])
         assert np.array_equal(ok, g["ok"][:, col]) and np.array_equal(d, g["d"][:, col])
         assert np.array_equal(it, g["it"][:, col])
+
+
+def test_full_size_bench_slice_equals_oracle():
+    """BASELINE configs[2] at its full per-GPU size (2^40 exp arguments,
+    65,536 super-domains, 2^25 domains): the device funnel's counts, failing
+    ids and candidates equal the CPU oracle's, and 8 logical shards of the
+    same slice reproduce them in order (size-independent properties)."""
+    import os
+
+    from paper_1211_3056_b200.device import DeviceSlice, FusedRunner
+    from paper_1211_3056_b200.shard import partition_blocks
+    from paper_1211_3056_b200.slices import slice_view
+
+    oracle.set_threads(os.cpu_count() or 1)
+    batch, cfg = _big_slice("exp", 0, 40, 32)
+    run = FusedRunner(DeviceSlice(batch), 2, 1, 8, sub_cap=batch.n_total // 4, cand_cap=1 << 16)
+    run.launch()
+    r = run.result()
+    fails = oracle.phase1(batch, "regular", 1)
+    assert np.array_equal(r.fail_ids + np.uint64(batch.id0), fails)
+    rows = oracle.phase2(batch, "regular", 1, 8, fails)
+    m, dist, dom = oracle.phase3(batch, rows)
+    assert len(r.sub_keys) == len(rows[0])
+    assert np.array_equal(r.cand_index, m) and np.array_equal(r.cand_dist, dist)
+    cands = []
+    for t0, t1 in partition_blocks([s.count for s in batch.supers], 8):
+        sub = slice_view(batch, t0, t1)
+        fr = FusedRunner(DeviceSlice(sub), 2, 1, 8, sub_cap=sub.n_total // 4, cand_cap=1 << 16)
+        fr.launch()
+        cands.append(fr.result().cand_index)
+    assert np.array_equal(np.concatenate(cands), m)
