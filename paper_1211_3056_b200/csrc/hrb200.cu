@@ -1530,14 +1530,19 @@ int hrb_run_slice_host(const hrb_slice* hs, int algo, int mode, int split, uint6
         CK(cudaMallocHost((void**)&H.hcount, sizeof(uint64_t)));
     }
     const int64_t S = hs->n_super, CL = hs->coef_limbs, NT = hs->n_total;
-    const size_t b_coef = sizeof(uint32_t) * 6 * CL * S, b2 = sizeof(uint64_t) * 2 * S, b32 = sizeof(uint32_t) * S;
+    // the phases read coefficients only mod 2^128: with >= 4 two's-complement
+    // limbs, only the low four of each coefficient are uploaded
+    const int64_t CLd = CL >= 4 ? 4 : CL;
+    const size_t b_coef = sizeof(uint32_t) * 6 * CLd * S, b2 = sizeof(uint64_t) * 2 * S, b32 = sizeof(uint32_t) * S;
     if ((rc = H.coef.ensure(b_coef)) || (rc = H.G.ensure(b2)) || (rc = H.s2.ensure(b2)) || (rc = H.nd.ensure(b32)) ||
         (rc = H.dn.ensure(b32)) || (rc = H.ln.ensure(b32)) || (rc = H.db.ensure(sizeof(uint64_t) * (S + 1))) ||
         (rc = H.m0.ensure(sizeof(uint64_t) * S)) || (rc = H.counts.ensure(sizeof(uint64_t) * 4)))
         return rc;
     cudaStream_t st = H.st;
     CK(cudaEventRecord(H.e0, st));
-    CK(cudaMemcpyAsync(H.coef.p, hs->coef, b_coef, cudaMemcpyHostToDevice, st));
+    for (int c = 0; c < 6; c++)  // rows c*CL .. c*CL + CLd - 1 are contiguous in the host layout
+        CK(cudaMemcpyAsync((uint32_t*)H.coef.p + (int64_t)c * CLd * S, hs->coef + (int64_t)c * CL * S,
+                           sizeof(uint32_t) * CLd * S, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(H.G.p, hs->G, b2, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(H.s2.p, hs->s2abs, b2, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(H.nd.p, hs->n_dom, b32, cudaMemcpyHostToDevice, st));
@@ -1547,6 +1552,7 @@ int hrb_run_slice_host(const hrb_slice* hs, int algo, int mode, int split, uint6
     CK(cudaMemcpyAsync(H.m0.p, hs->m0, sizeof(uint64_t) * S, cudaMemcpyHostToDevice, st));
     hrb_slice ds = *hs;
     ds.coef = (const uint32_t*)H.coef.p;
+    ds.coef_limbs = (int32_t)CLd;
     ds.G = (const uint64_t*)H.G.p;
     ds.s2abs = (const uint64_t*)H.s2.p;
     ds.n_dom = (const uint32_t*)H.nd.p;

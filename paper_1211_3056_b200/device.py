@@ -224,7 +224,11 @@ class HostRunner:
         self.cm, self.cd, self.cdom = (b.numpy().view(np.uint64) for b in bufs)
 
     def input_bytes(self) -> int:
-        return sum(v.nbytes for v in self.inputs.values())
+        """Bytes hrb_run_slice_host copies host -> device per call (coefficients
+        travel as their low four limbs, the residues the phases read)."""
+        cl = self.batch.coef_limbs
+        coef = self.inputs["coef"].nbytes * min(cl, 4) // cl
+        return coef + sum(v.nbytes for k, v in self.inputs.items() if k != "coef")
 
     def run(self):
         """One end-to-end call; returns (counts, fail_ids, cand_index,
