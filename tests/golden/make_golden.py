@@ -243,8 +243,8 @@ def _reference_slice(fn, binade, cfg, s_lo, s_cnt):
 
 
 def _cfg(fn, p, eps_bits, tau, N, mu, nu, algorithm="regular", div_mode="hybrid", split=8,
-         word_bits=64, delta=2):
-    pg = PolyGenConfig(tau=tau, N=N, mu=mu, nu=nu, delta=delta, limbs=8, frac_bits=96, guard=32)
+         word_bits=64, delta=2, frac_bits=96):
+    pg = PolyGenConfig(tau=tau, N=N, mu=mu, nu=nu, delta=delta, limbs=8, frac_bits=frac_bits, guard=32)
     ph = PhaseConfig(algorithm=algorithm, div_mode=MODES[div_mode], phase2_split=split, N1=N)
     return PipelineConfig(fn=fn, fmt=FpFormat(p, eps_bits), polygen=pg, phase=ph, word_bits=word_bits)
 
@@ -262,7 +262,7 @@ def _case(name, fn, binade, p, eps_bits, tau, N, mu, nu, s_lo, s_cnt, **kw):
     out.update({"name": name, "fn": fn, "binade": binade, "p": p, "eps_bits": eps_bits,
                 "slice": [s_lo, s_cnt],
                 "cfg": {"tau": tau, "N": N, "mu": mu, "nu": nu, "delta": kw.get("delta", 2),
-                        "limbs": 8, "frac_bits": 96, "guard": 32,
+                        "limbs": 8, "frac_bits": kw.get("frac_bits", 96), "guard": 32,
                         "algorithm": kw.get("algorithm", "regular"),
                         "div_mode": kw.get("div_mode", "hybrid"), "split": kw.get("split", 8),
                         "word_bits": kw.get("word_bits", 64)}})
@@ -304,9 +304,41 @@ def pipeline_goldens():
     print("wrote pipeline_cases.json")
 
 
+def extra_goldens():
+    """Cases appended to pipeline_cases.json: other grid widths F (the
+    device's 128-bit phase-3 path runs for F > 96), a wider phase-2 split,
+    exp2 and the classic walk's other division modes at binary64."""
+    path = os.path.join(HERE, "pipeline_cases.json")
+    with open(path) as fh:
+        cases = json.load(fh)
+    have = {c["name"] for c in cases}
+    extra = [
+        ("p53_exp_F128", dict(fn="exp", binade=0, p=53, eps_bits=16, tau=64, N=1 << 12, mu=8, nu=8, s_lo=0,
+                              s_cnt=1 << 20, frac_bits=128)),
+        ("p53_exp_F64", dict(fn="exp", binade=0, p=53, eps_bits=16, tau=64, N=1 << 12, mu=8, nu=8, s_lo=0,
+                             s_cnt=1 << 20, frac_bits=64)),
+        ("p53_exp_split16", dict(fn="exp", binade=0, p=53, eps_bits=16, tau=8, N=1 << 15, mu=2, nu=4, s_lo=0,
+                                 s_cnt=1 << 20, split=16)),
+        ("p53_exp2_e16", dict(fn="exp2", binade=0, p=53, eps_bits=16, tau=8, N=1 << 15, mu=2, nu=4, s_lo=0,
+                              s_cnt=1 << 20)),
+        ("p53_exp_lef_hw", dict(fn="exp", binade=0, p=53, eps_bits=16, tau=64, N=1 << 12, mu=8, nu=8, s_lo=0,
+                                s_cnt=1 << 20, algorithm="lefevre", div_mode="hw")),
+    ]
+    for name, kw in extra:
+        if name in have:
+            continue
+        args = [kw.pop(k) for k in ("fn", "binade", "p", "eps_bits", "tau", "N", "mu", "nu", "s_lo", "s_cnt")]
+        cases.append(_case(name, *args, **kw))
+    with open(path, "w") as fh:
+        json.dump(cases, fh, separators=(",", ":"))
+    print("wrote pipeline_cases.json")
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["search", "pipeline"]
+    which = sys.argv[1:] or ["search", "pipeline", "extra"]
     if "search" in which:
         search_goldens()
     if "pipeline" in which:
         pipeline_goldens()
+    if "extra" in which:
+        extra_goldens()

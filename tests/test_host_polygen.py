@@ -12,7 +12,8 @@ from paper_1211_3056_b200.slices import build_super_domains
 
 
 @pytest.mark.parametrize("name", ["p13_exp_b0", "p13_log_b0", "p13_exp2_b1", "p13_exp_b-1",
-                                  "p53_exp_2p20_e16_N15", "p53_exp_ragged", "p53_log_sqrt2_e16", "p53_exp_delta1"])
+                                  "p53_exp_2p20_e16_N15", "p53_exp_ragged", "p53_log_sqrt2_e16", "p53_exp_delta1",
+                                  "p53_exp_F128", "p53_exp_F64", "p53_exp2_e16"])
 def test_super_domains_match_reference(name):
     c = case(name)
     cfg = config_of(c)
