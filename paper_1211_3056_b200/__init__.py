@@ -50,6 +50,7 @@ from .funnel import (
     prepare_slice,
     execute_batch,
     run_pipeline,
+    run_range,
     run_slice,
     select_algorithm,
 )
@@ -124,6 +125,6 @@ __all__ = [
     "float_bits", "forward_difference", "frac_div", "hierarchical_split", "is_hr_case", "lefevre_lb",
     "lefevre_swap_lb", "mantissa_exponent", "newton_interpolate", "output_binade_pieces", "pack_slice",
     "phase1", "phase2", "phase3_exhaustive", "prepare_slice", "regular_lb", "regular_unrolled_lb",
-    "run_pipeline", "run_slice", "search_many", "select_algorithm", "split_binade", "straightforward_shift",
+    "run_pipeline", "run_range", "run_slice", "search_many", "select_algorithm", "split_binade", "straightforward_shift",
     "tabulated_shift_step", "taylor_approx", "value_exponent",
 ]

@@ -251,6 +251,63 @@ def run_pipeline(binade: int, cfg: PipelineConfig, prev_stats: PhaseStats | None
     return out.records, out.stats
 
 
+@dataclass
+class RangeOutput:
+    """run_range's result: records of the whole range (ascending) and one
+    PhaseStats per interval, with the algorithm each interval used."""
+
+    records: list
+    interval_stats: list
+    choices: list  # (first argument index, algorithm) per interval
+
+
+def run_range(fn: str, binade: int, start: int, count: int, cfg: PipelineConfig, interval_args: int = 1 << 36,
+              workers: int | None = None, confirm: bool = True) -> RangeOutput:
+    """A long argument range as consecutive intervals, the way the paper walks
+    a binade: the block schedule of the WHOLE range is
+    planned once (so blocks, domain ids and results are exactly those of a
+    single run_slice), cut into intervals of about `interval_args`
+    arguments, and with algorithm "auto" each interval's search family is
+    chosen from the previous interval's funnel (select_algorithm,
+    pipeline.py:187-197).  The host Taylor generation of interval i+1 runs in
+    a background thread while the device and the host confirmation work on
+    interval i."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from .shard import partition_blocks
+    from .slices import pack_slice, plan_blocks, supers_of_blocks
+
+    w = workers if workers is not None else cfg.phase.parallel_width
+    blocks = plan_blocks(fn, binade, cfg.fmt, cfg.polygen, start, count)
+    sizes = [b.bcount for b in blocks]
+    n_int = max(1, -(-sum(sizes) // max(1, interval_args)))
+    parts = [p for p in partition_blocks(sizes, n_int) if p[1] > p[0]]
+    ceiling = cfg.phase.budgets.eps_dprime if cfg.phase.budgets is not None else None
+
+    def prepare(part):
+        supers = supers_of_blocks(blocks[part[0]:part[1]], w)
+        return pack_slice(supers, cfg.fmt, cfg.polygen, cfg.word_bits, binade, budget_ceiling=ceiling)
+
+    records, stats_list, choices = [], [], []
+    prev = None
+    with ThreadPoolExecutor(max_workers=1) as ex:
+        nxt = ex.submit(prepare, parts[0]) if parts else None
+        for k, part in enumerate(parts):
+            batch = nxt.result()
+            nxt = ex.submit(prepare, parts[k + 1]) if k + 1 < len(parts) else None
+            algo = cfg.phase.algorithm
+            if algo == "auto":
+                algo = select_algorithm(prev)
+            out = execute_batch(batch, cfg, algo, fn, confirm=confirm)
+            out.stats.algorithm_choices.append((blocks[part[0]].bstart, algo))
+            records.extend(out.records)
+            stats_list.append(out.stats)
+            choices.append((blocks[part[0]].bstart, algo))
+            prev = out.stats
+    records.sort()
+    return RangeOutput(records, stats_list, choices)
+
+
 # --------------------------------------------------- per-phase drop-ins
 
 

@@ -365,3 +365,28 @@ def test_full_size_bench_slice_equals_oracle():
         fr.launch()
         cands.append(fr.result().cand_index)
     assert np.array_equal(np.concatenate(cands), m)
+
+
+def test_run_range_intervals_equal_one_slice_and_switch_algorithms():
+    """run_range cuts the planned block schedule into intervals: records
+    equal one run_slice of the whole range (and the reference's golden
+    records), and "auto" picks each interval's search from the previous
+    interval's funnel."""
+    from dataclasses import replace
+
+    from paper_1211_3056_b200.funnel import run_range, run_slice
+
+    c = case("p53_exp_2p20_e16_N12")
+    cfg = config_of(c)
+    lo, cnt = c["slice"]
+    whole = run_slice(c["fn"], c["binade"], lo, cnt, cfg)
+    out = run_range(c["fn"], c["binade"], lo, cnt, cfg, interval_args=1 << 18, workers=2)
+    assert essence(out.records) == essence(whole.records) == c["records"]
+    assert len(out.interval_stats) == 4
+    auto = replace(cfg, phase=replace(cfg.phase, algorithm="auto"))
+    out2 = run_range(c["fn"], c["binade"], lo, cnt, auto, interval_args=1 << 18, workers=2)
+    assert essence(out2.records) == c["records"]
+    assert out2.choices[0][1] == "regular"  # no previous interval
+    for k in range(1, len(out2.choices)):
+        ratio = out2.interval_stats[k - 1].phase3_phase1_ratio()
+        assert out2.choices[k][1] == ("lefevre" if ratio > 1e-3 else "regular")
