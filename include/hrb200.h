@@ -162,7 +162,9 @@ int hrb_phase3(const hrb_slice* s, int split, const uint64_t* sub_keys, const ui
 
 /*
  * The three phases back to back on the device (the north-star hot path for
- * one slice); no host synchronisation between phases.  counts (device
+ * one slice); no host synchronisation between phases.  A call repeating the
+ * previous call's arguments exactly (same slice, outputs, algorithm) replays
+ * the captured launch sequence as one CUDA graph (HRB_NO_GRAPH=1 disables).  counts (device
  * uint64[4]): phase-1 fails, phase-2 survivors, phase-3 candidates,
  * phase-1 iteration sum.  Capacities: fail_cap, sub_cap, cand_cap.
  */

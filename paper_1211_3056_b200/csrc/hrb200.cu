@@ -310,14 +310,16 @@ struct Walk {  // per-lane stride-32 difference tables, in shared memory
 };
 
 // top W bits of (x mod 2^F), i.e. (x mod 2^F) >> (F - W), via one funnel
-// shift: sh = 128 - F
-template <int W>
+// shift: sh = 128 - F.  SH >= 0 fixes the shift at compile time (the
+// pipeline's F = 96: a register pick and one funnel shift instead of a
+// variable 128-bit shift).
+template <int W, int SH = -1>
 __device__ __forceinline__ uint64_t top_bits(u128 x, int sh) {
-    const u128 y = x << sh;
+    const u128 y = SH >= 0 ? x << SH : x << sh;
     return W == 64 ? (uint64_t)(y >> 64) : (uint64_t)(y >> 96);
 }
 
-template <int W>
+template <int W, int SH = -1>
 struct WalkSrc {
     Walk* w;
     const u128* inc;  // per-warp constants in shared memory: {g2, h1}
@@ -331,8 +333,8 @@ struct WalkSrc {
         const u128 s0 = w->g0, s1 = w->h0, g1 = w->g1;
         const uint64_t pad = last ? pad_last : pad_full;
         const uint64_t wmask = W == 64 ? ~0ull : 0xFFFFFFFFull;
-        a = top_bits<W>(0 - s1, sh);
-        b = (top_bits<W>(s0, sh) + pad) & wmask;
+        a = top_bits<W, SH>(0 - s1, sh);
+        b = (top_bits<W, SH>(s0, sh) + pad) & wmask;
         eps = 2 * pad;
         N = last ? nlast : nfull;
         // tabulated step: three multi-word additions per domain
@@ -344,7 +346,7 @@ struct WalkSrc {
     __device__ __forceinline__ void done(int, bool, uint64_t, uint32_t) {}
 };
 
-template <int W>
+template <int W, int SH>
 __global__ void __launch_bounds__(128, HRB_P1_MINB) phase1_reg_kernel(SliceDev s, int algo, const uint64_t* tile_base,
                                                           uint32_t* bitmap, uint32_t* tile_t,
                                                           unsigned long long* iter_sum) {
@@ -355,7 +357,7 @@ __global__ void __launch_bounds__(128, HRB_P1_MINB) phase1_reg_kernel(SliceDev s
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const uint64_t total_tiles = tile_base[s.S];
     unsigned long long iters = 0;
-    WalkSrc<W> src;
+    WalkSrc<W, SH> src;
     src.w = &walks[threadIdx.x];
     src.inc = incs[threadIdx.x >> 5];
     src.sh = 128 - s.F;
@@ -402,7 +404,7 @@ __global__ void __launch_bounds__(128, HRB_P1_MINB) phase1_reg_kernel(SliceDev s
 // lane's items.  The shifted polynomials (straightforward_shift by j*step,
 // polygen.py:143-158) are walked with tabulated differences of stride
 // `step`: t0 += dt0, dt0 += s2 step^2, t1 += s2 step (exact mod 2^128).
-template <int W>
+template <int W, int SH = -1>
 struct SubWalkSrc {
     u128 t0, dt0, d2, t1, dt1;
     uint64_t pad_full, pad_last;
@@ -414,8 +416,8 @@ struct SubWalkSrc {
         const bool last = j == nsub - 1;
         const uint64_t pad = last ? pad_last : pad_full;
         const uint64_t wmask = W == 64 ? ~0ull : 0xFFFFFFFFull;
-        a = top_bits<W>(0 - t1, sh);
-        b = (top_bits<W>(t0, sh) + pad) & wmask;
+        a = top_bits<W, SH>(0 - t1, sh);
+        b = (top_bits<W, SH>(t0, sh) + pad) & wmask;
         eps = 2 * pad;
         N = last ? last_cnt : step;
         t0 += dt0;
@@ -426,7 +428,7 @@ struct SubWalkSrc {
     __device__ __forceinline__ void done(int, bool, uint64_t, uint32_t) {}
 };
 
-template <int W>
+template <int W, int SH>
 __global__ void __launch_bounds__(128, HRB_P2_MINB) phase2_reg_kernel(SliceDev s, int split, const uint64_t* fail_ids,
                                                           const uint32_t* fail_t, const uint64_t* fail_count,
                                                           uint64_t fail_cap, const unsigned long long* meta,
@@ -435,7 +437,7 @@ __global__ void __launch_bounds__(128, HRB_P2_MINB) phase2_reg_kernel(SliceDev s
     if (nf > fail_cap) nf = fail_cap;
     const uint32_t J = (uint32_t)meta[0];
     const uint32_t wpd = (J + 31) >> 5;  // bitmap words per failing domain
-    SubWalkSrc<W> src;
+    SubWalkSrc<W, SH> src;
     src.sh = 128 - s.F;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     // whole warps iterate together so the lockstep pairs stay converged
@@ -1152,8 +1154,9 @@ int phase1_impl(Workspace& ws, const hrb_slice* s, const SliceDev& sd, int algo,
     auto is = (unsigned long long*)iter_sum;
     if (algo >= hrb::ALGO_REGULAR) {
         const int g5 = sm_count() * HRB_P1_MINB;  // persistent: one wave at the launch bound
-        if (sd.W == 64) phase1_reg_kernel<64><<<g5, 128, 0, st>>>(sd, algo, tb, bm, tt, is);
-        else phase1_reg_kernel<32><<<g5, 128, 0, st>>>(sd, algo, tb, bm, tt, is);
+        if (sd.W == 64 && sd.F == 96) phase1_reg_kernel<64, 32><<<g5, 128, 0, st>>>(sd, algo, tb, bm, tt, is);
+        else if (sd.W == 64) phase1_reg_kernel<64, -1><<<g5, 128, 0, st>>>(sd, algo, tb, bm, tt, is);
+        else phase1_reg_kernel<32, -1><<<g5, 128, 0, st>>>(sd, algo, tb, bm, tt, is);
     } else {
         if (sd.W == 64) phase1_kernel<64, false><<<grid, 256, 0, st>>>(sd, algo, mode, tb, bm, tt, is);
         else phase1_kernel<32, false><<<grid, 256, 0, st>>>(sd, algo, mode, tb, bm, tt, is);
@@ -1182,8 +1185,12 @@ int phase2_impl(Workspace& ws, const hrb_slice* s, const SliceDev& sd, int algo,
     auto bm = (uint32_t*)ws.bm2.p;
     if (algo >= hrb::ALGO_REGULAR) {
         const int g4 = sm_count() * HRB_P2_MINB * 4;  // grid-stride over failing domains (device count)
-        if (sd.W == 64) phase2_reg_kernel<64><<<g4, 128, 0, st>>>(sd, split, fail_ids, fail_t, fail_count, fail_cap, mt, bm);
-        else phase2_reg_kernel<32><<<g4, 128, 0, st>>>(sd, split, fail_ids, fail_t, fail_count, fail_cap, mt, bm);
+        if (sd.W == 64 && sd.F == 96)
+            phase2_reg_kernel<64, 32><<<g4, 128, 0, st>>>(sd, split, fail_ids, fail_t, fail_count, fail_cap, mt, bm);
+        else if (sd.W == 64)
+            phase2_reg_kernel<64, -1><<<g4, 128, 0, st>>>(sd, split, fail_ids, fail_t, fail_count, fail_cap, mt, bm);
+        else
+            phase2_reg_kernel<32, -1><<<g4, 128, 0, st>>>(sd, split, fail_ids, fail_t, fail_count, fail_cap, mt, bm);
     } else {
         if (sd.W == 64)
             phase2_classic_kernel<64><<<grid, 256, 0, st>>>(sd, mode, split, fail_ids, fail_t, fail_count, fail_cap, mt, bm);
