@@ -349,7 +349,7 @@ def main():
                      for b, d, i in zip(bits, res.cand_dist.tolist(), res.cand_dom.tolist())],
                     dtype=np.uint64).reshape(-1, 4)
     local_res = ShardResult(np.array([counts[0], counts[1], counts[2], 0, counts[3], count], dtype=np.int64), cand)
-    t_all = torch.tensor([ms, float(np.mean(p1_ms)), e2e["ms_per_step"] if e2e else 0.0],
+    t_all = torch.tensor([ms, float(np.median(p1_ms)), e2e["ms_per_step"] if e2e else 0.0],
                          device="cpu" if one_dev else "cuda")
     gather_ms = 0.0
     if dist:
@@ -393,6 +393,7 @@ def main():
                 "hbm": hbm_side(k1.get("dram_bytes_per_launch"), p1_max),
                 "algorithmic_unit": "CF quotient step (SearchOutcome.iterations)",
                 "quotient_steps_per_launch": iters, "kernel_ms": p1_max,
+                "kernel_ms_samples": [round(x, 4) for x in p1_ms],
                 "quotient_steps_per_s": iters / (p1_max / 1e3),
                 "int_lane_instr_per_quotient_step": lane_per_step,
                 "calibration": os.path.relpath(CALIBRATION, ROOT) if k1 else None,
