@@ -64,6 +64,12 @@ int cuda_err(cudaError_t e, const char* where) {
 #ifndef HRB_P2_MINB
 #define HRB_P2_MINB 5
 #endif
+#ifndef HRB_P1_DYN
+#define HRB_P1_DYN 1  // phase-1 regular kernel: dynamic tile scheduler
+#endif
+#ifndef HRB_P2_DYN
+#define HRB_P2_DYN 1  // phase-2 regular kernel: dynamic chunk scheduler
+#endif
 #ifndef HRB_NU
 #define HRB_NU 16
 #endif
@@ -346,10 +352,18 @@ struct WalkSrc {
     __device__ __forceinline__ void done(int, bool, uint64_t, uint32_t) {}
 };
 
+// Tiles are handed out dynamically: a warp starts on tile warp0 and takes
+// each further tile from a device counter (tile_ctr, zeroed by ws_prep),
+// fetched one tile ahead so the atomic's latency hides behind the search.
+// Per-tile times vary with the domains' iteration counts and rare exact
+// repairs; a static grid-stride split left ~17 % of the warp slots idle at
+// the end of the kernel.  The bitmap and tile_t are indexed by tile, so the
+// output does not depend on which warp ran which tile.
 template <int W, int SH>
 __global__ void __launch_bounds__(128, HRB_P1_MINB) phase1_reg_kernel(SliceDev s, int algo, const uint64_t* tile_base,
                                                           uint32_t* bitmap, uint32_t* tile_t,
-                                                          unsigned long long* iter_sum) {
+                                                          unsigned long long* iter_sum,
+                                                          unsigned long long* tile_ctr) {
     __shared__ Walk walks[128];
     __shared__ u128 incs[4][2];
     const int lane = threadIdx.x & 31;
@@ -361,7 +375,14 @@ __global__ void __launch_bounds__(128, HRB_P1_MINB) phase1_reg_kernel(SliceDev s
     src.w = &walks[threadIdx.x];
     src.inc = incs[threadIdx.x >> 5];
     src.sh = 128 - s.F;
+#if HRB_P1_DYN
+    uint64_t gw = warp0;
+    while (gw < total_tiles) {
+        unsigned long long next = 0;
+        if (lane == 0) next = nwarps + atomicAdd(tile_ctr, 1ull);
+#else
     for (uint64_t gw = warp0; gw < total_tiles; gw += nwarps) {
+#endif
         const int64_t t = locate_super(tile_base, s.S, gw);
         const uint64_t tile = gw - tile_base[t];
         const u128 c00 = coef_res(s, t, 0), c01 = coef_res(s, t, 1), c02 = coef_res(s, t, 2);
@@ -395,6 +416,9 @@ __global__ void __launch_bounds__(128, HRB_P1_MINB) phase1_reg_kernel(SliceDev s
         }
         if (lane < NU) bitmap[gw * NU + lane] = mine;
         if (lane == 0) tile_t[gw] = (uint32_t)t;
+#if HRB_P1_DYN
+        gw = __shfl_sync(0xffffffffu, next, 0);
+#endif
     }
     for (int o = 16; o > 0; o >>= 1) iters += __shfl_xor_sync(0xffffffffu, iters, o);
     if (iter_sum && lane == 0 && iters) atomicAdd(iter_sum, iters);
@@ -431,7 +455,7 @@ struct SubWalkSrc {
 template <int W, int SH>
 __global__ void __launch_bounds__(128, HRB_P2_MINB) phase2_reg_kernel(SliceDev s, int split, const uint64_t* fail_ids,
                                                           const uint32_t* fail_t, const uint64_t* fail_count,
-                                                          uint64_t fail_cap, const unsigned long long* meta,
+                                                          uint64_t fail_cap, unsigned long long* meta,
                                                           uint32_t* bitmap) {
     uint64_t nf = *fail_count;
     if (nf > fail_cap) nf = fail_cap;
@@ -439,10 +463,23 @@ __global__ void __launch_bounds__(128, HRB_P2_MINB) phase2_reg_kernel(SliceDev s
     const uint32_t wpd = (J + 31) >> 5;  // bitmap words per failing domain
     SubWalkSrc<W, SH> src;
     src.sh = 128 - s.F;
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     // whole warps iterate together so the lockstep pairs stay converged
     const uint64_t nf_pad = (nf + 31) & ~31ull;
+#if HRB_P2_DYN
+    // a warp takes 32 consecutive failing domains at a time, the first chunk
+    // by its id and the rest from a device counter (meta[5], zeroed by
+    // ws_prep), fetched one chunk ahead (see phase1_reg_kernel)
+    const int lane = threadIdx.x & 31;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    uint64_t chunk = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    while (32 * chunk < nf_pad) {
+        unsigned long long next = 0;
+        if (lane == 0) next = nwarps + atomicAdd(&meta[5], 1ull);
+        const uint64_t f = 32 * chunk + lane;
+#else
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t f = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; f < nf_pad; f += stride) {
+#endif
         const bool valid = f < nf;
         src.nsub = 0;
         if (valid) {
@@ -477,6 +514,9 @@ __global__ void __launch_bounds__(128, HRB_P2_MINB) phase2_reg_kernel(SliceDev s
             const uint32_t fails = hrb::lane_items<W, 32>(src, &its, false, src.nsub > 32 * c ? src.nsub - 32 * c : 0);
             if (valid) bitmap[f * wpd + c] = fails;
         }
+#if HRB_P2_DYN
+        chunk = __shfl_sync(0xffffffffu, next, 0);
+#endif
     }
 }
 
@@ -1115,8 +1155,10 @@ int ws_prep(Workspace& ws, const SliceDev& sd, int split, cudaStream_t st) {
     int rc;
     if ((rc = ws.tiles.ensure(sizeof(uint64_t) * (S + 1)))) return rc;
     if ((rc = ws.tile_base.ensure(sizeof(uint64_t) * (S + 1)))) return rc;
-    if ((rc = ws.meta.ensure(sizeof(unsigned long long) * 4))) return rc;
-    CK(cudaMemsetAsync(ws.meta.p, 0, sizeof(unsigned long long) * 4, st));
+    // meta: [0] J, [1] max subdomain step, [2] phase-3 chunk, [4] phase-1 tile counter,
+    // [5] phase-2 chunk counter
+    if ((rc = ws.meta.ensure(sizeof(unsigned long long) * 8))) return rc;
+    CK(cudaMemsetAsync(ws.meta.p, 0, sizeof(unsigned long long) * 8, st));
     prep_kernel<<<(unsigned)((S + 1 + 255) / 256), 256, 0, st>>>(sd, split, (uint64_t*)ws.tiles.p,
                                                                  (unsigned long long*)ws.meta.p);
     CK(cudaGetLastError());
@@ -1152,11 +1194,12 @@ int phase1_impl(Workspace& ws, const hrb_slice* s, const SliceDev& sd, int algo,
     auto bm = (uint32_t*)ws.bm1.p;
     auto tt = (uint32_t*)ws.tile_t.p;
     auto is = (unsigned long long*)iter_sum;
+    auto tc = (unsigned long long*)ws.meta.p + 4;
     if (algo >= hrb::ALGO_REGULAR) {
         const int g5 = sm_count() * HRB_P1_MINB;  // persistent: one wave at the launch bound
-        if (sd.W == 64 && sd.F == 96) phase1_reg_kernel<64, 32><<<g5, 128, 0, st>>>(sd, algo, tb, bm, tt, is);
-        else if (sd.W == 64) phase1_reg_kernel<64, -1><<<g5, 128, 0, st>>>(sd, algo, tb, bm, tt, is);
-        else phase1_reg_kernel<32, -1><<<g5, 128, 0, st>>>(sd, algo, tb, bm, tt, is);
+        if (sd.W == 64 && sd.F == 96) phase1_reg_kernel<64, 32><<<g5, 128, 0, st>>>(sd, algo, tb, bm, tt, is, tc);
+        else if (sd.W == 64) phase1_reg_kernel<64, -1><<<g5, 128, 0, st>>>(sd, algo, tb, bm, tt, is, tc);
+        else phase1_reg_kernel<32, -1><<<g5, 128, 0, st>>>(sd, algo, tb, bm, tt, is, tc);
     } else {
         if (sd.W == 64) phase1_kernel<64, false><<<grid, 256, 0, st>>>(sd, algo, mode, tb, bm, tt, is);
         else phase1_kernel<32, false><<<grid, 256, 0, st>>>(sd, algo, mode, tb, bm, tt, is);
@@ -1181,10 +1224,14 @@ int phase2_impl(Workspace& ws, const hrb_slice* s, const SliceDev& sd, int algo,
         fail_t = (const uint32_t*)ws.fail_t.p;
     }
     const int grid = sm_count() * 8;
-    auto mt = (const unsigned long long*)ws.meta.p;
+    auto mt = (unsigned long long*)ws.meta.p;
     auto bm = (uint32_t*)ws.bm2.p;
     if (algo >= hrb::ALGO_REGULAR) {
+#if HRB_P2_DYN
+        const int g4 = sm_count() * HRB_P2_MINB;  // persistent: one wave, chunks from the counter
+#else
         const int g4 = sm_count() * HRB_P2_MINB * 4;  // grid-stride over failing domains (device count)
+#endif
         if (sd.W == 64 && sd.F == 96)
             phase2_reg_kernel<64, 32><<<g4, 128, 0, st>>>(sd, split, fail_ids, fail_t, fail_count, fail_cap, mt, bm);
         else if (sd.W == 64)
