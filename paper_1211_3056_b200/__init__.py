@@ -66,6 +66,7 @@ from .search import (
     regular_unrolled_lb,
     search_many,
 )
+from .records import emit_records, emit_stats, record_dict, write_records
 from .slices import SliceBatch, SuperDomain, build_super_domains, output_binade_pieces, pack_slice
 from .taylor import (
     BinomialPoly,
@@ -115,6 +116,7 @@ def domain_coefficient_sets(r_polys, cfg: PolyGenConfig) -> list[tuple]:
 
 
 __all__ = [
+    "emit_records", "emit_stats", "record_dict", "write_records",
     "BRANCH_WEIGHTS", "BranchWeights", "DivergenceReport", "WarpStats", "WarpTrace", "branch_serialization_estimate",
     "linear_problem_batch", "mdm", "measure_warps", "nmdm", "simulate_warps",
     "Algorithm", "BinadeDomains", "BinomialPoly", "DivisionMode", "Domain", "DomainTask", "ErrorBudget",
