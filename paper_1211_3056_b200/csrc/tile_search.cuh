@@ -27,12 +27,13 @@ namespace hrb {
 // divisor (S) and B the dividend (L); the else-half replaces B by B mod A,
 // the following then-half replaces A by A mod B.  A loop iteration is one
 // (else, then) pair, so the state returns to the same registers with no
-// role-swap moves.  cA, cB are the matching point counts; Af, Bf the values
-// rounded to float (used only for quotient estimates).
+// role-swap moves.  cA, cB are the matching point counts and M the budget
+// left, N - cA - cB (>= 0 while the search runs); Af, Bf the values rounded
+// to float (quotient estimates, and the fast path's r < S and L == 0 tests).
 struct Slot {
     uint64_t A, B, d;
     float Af, Bf;
-    uint32_t cA, cB;
+    uint32_t cA, cB, M;
 };
 
 // floor(y/x + e) from the FP32 reciprocal in one round-down FFMA: with
@@ -53,7 +54,25 @@ __device__ __forceinline__ float rcp_approx(float x) {
     return r;
 }
 
+// x - y and whether it did not borrow (x >= y), from one carry chain: the
+// comparison the else-half needs comes free with the subtraction.
+__device__ __forceinline__ uint64_t sub_nb(uint64_t x, uint64_t y, bool& ge) {
+    uint32_t lo, hi, c;
+    asm("sub.cc.u32 %0, %3, %5;\n\t"
+        "subc.cc.u32 %1, %4, %6;\n\t"
+        "subc.u32 %2, 0, 0;"
+        : "=r"(lo), "=r"(hi), "=r"(c)
+        : "r"((uint32_t)x), "r"((uint32_t)(x >> 32)), "r"((uint32_t)y), "r"((uint32_t)(y >> 32)));
+    ge = c == 0;
+    return ((uint64_t)hi << 32) | lo;
+}
+
 constexpr int32_t QMAX = 1 << 20;
+
+// x + k * y mod 2^64 for a 32-bit k.  With y = -S precomputed once per
+// half-step, both of its products (L - k S and x - k2 S) compile to one wide
+// multiply-add on the low word and one multiply-add on the high word.
+__device__ __forceinline__ uint64_t madd64(uint64_t x, uint32_t k, uint64_t y) { return x + (uint64_t)k * y; }
 
 // One half-step, fast path: Lp = L mod S with its quotient k, and the
 // reduced d, from one FP32 reciprocal of S and round-down quotient estimates
@@ -61,47 +80,50 @@ constexpr int32_t QMAX = 1 << 20;
 // reference's `p < q` body (d %= p) versus the `p >= q` body (d reduced past
 // the new p; when d < Lp, d < S already and the mod is the identity).
 // `bad` flags a step the estimates may have got wrong -- a remainder outside
-// [0, S) or a quotient >= 2^20 -- which hs_exact redoes; nothing is fixed up
-// on the fast path.  Invariants on an active slot: S < L, d < L, S <= 2^63.
+// [0, S) or a quotient >= 2^20 -- which hs_redo redoes; nothing is fixed up
+// on the fast path.  r < S is proved in float: rounding is monotone, so
+// float(r) < float(S) implies r < S (equal floats are flagged, rarely and
+// harmlessly).  Invariants on an active slot: S < L, d < L, S <= 2^63.
 //
 // FIRST: the first step of a search, the only one whose divisor (a) may
 // exceed 2^63 and whose dividend (one - a) may be below it.  Its quotient
 // estimate is clamped at 0 and a wrapped subtraction is caught directly
 // (result above its minuend), since ">= S" no longer implies a wrap there.
 template <bool THEN, bool FIRST = false>
-__device__ __forceinline__ void hs_fast(uint64_t& L, uint64_t S, float Lf, float Sf, uint64_t& d, uint32_t& k,
+__device__ __forceinline__ void hs_fast(uint64_t& L, uint64_t S, float& Lf, float Sf, uint64_t& d, uint32_t& k,
                                         uint32_t& k2, bool& sub, bool& bad) {
     const float rcp = rcp_approx(Sf);
     // floor(L/S) >= 1 except on a first step, so the estimate is >= 0
     const int32_t ke = FIRST ? max(qfloor(Lf, rcp), 0) : qfloor(Lf, rcp);
-    const uint64_t r = L - (uint64_t)(uint32_t)ke * S;
+    const uint64_t nS = 0 - S;
+    const uint64_t r = madd64(L, (uint32_t)ke, nS);
     uint64_t x = d;
-    sub = !THEN && x >= r;
-    if (sub) x -= r;
+    if (THEN) {
+        sub = false;
+    } else {
+        const uint64_t t = sub_nb(d, r, sub);
+        x = sub ? t : d;
+    }
     // the quotient of x by S is >= 0; an estimate of -1 (x/S within |e| of
     // 0 from above) is clamped to 0, which is then exact
     const uint32_t ke2 = (uint32_t)max(qfloor(__ull2float_rn(x), rcp), 0);
-    const uint64_t y = x - (uint64_t)ke2 * S;
-    bad = (ke >= QMAX) | (r >= S) | (y >= S);
+    const uint64_t y = madd64(x, ke2, nS);
+    const float rf = __ull2float_rn(r);
+    bad = (ke >= QMAX) | !(rf < Sf) | (y >= S);
     if (FIRST) bad |= (r > L) | (y > x);
     // in place: the old L and d are recoverable from (r, y, ke, ke2, sub)
     // on the exact path, so no copy of them stays live across the vote
     L = r;
+    Lf = rf;
     d = y;
     k = (uint32_t)ke;
     k2 = ke2;
 }
 
-// Undo hs_fast's in-place update (all arithmetic mod 2^64 is exact) and
-// redo the half-step with hardware division.
-__device__ __forceinline__ void hs_redo(uint64_t& L, uint64_t S, uint64_t& d, uint32_t& k, uint32_t k2, bool sub,
-                                        bool then_body);
-
-
 // The same half-step with hardware 64-bit division (rare: a quotient >= 2^20
 // or an estimate that missed by one).
 // k saturates at 2^32 - 1: any quotient that large ends the search (cS >= 1
-// makes cLp >= 2^32 - 1 >= N - cS), exactly as the reference's u + v >= N.
+// makes k cS >= 2^32 - 1 >= M), exactly as the reference's u + v >= N.
 // Out of line and by value, so the hot loop keeps its registers.
 struct ExactStep {
     uint64_t Lp, dn;
@@ -118,24 +140,28 @@ __device__ __noinline__ ExactStep hs_exact(uint64_t L, uint64_t S, uint64_t d, b
     return e;
 }
 
-// Finish a half-step (L and d already updated in place): cL <- k cS + cL and
-// the float copy of L, and report whether the search ended: expansion
-// exhausted (L == 0) or the count reaches N.  A finished slot keeps
-// computing harmless garbage.
-__device__ __forceinline__ bool hs_commit(uint64_t L, float& Lf, uint32_t& cL, uint32_t cS, uint32_t N, uint32_t k) {
-    const uint64_t cLp = (uint64_t)k * cS + cL;
-    const bool done = L == 0 || cLp >= (uint64_t)(N - cS);
-    Lf = __ull2float_rn(L);
-    cL = (uint32_t)cLp;
+// Finish a half-step (L, Lf and d already updated): cL <- k cS + cL, and
+// report whether the search ended: expansion exhausted (L == 0, i.e.
+// Lf == 0) or the count reaches N, i.e. k cS >= M = N - cL - cS (the
+// reference's u + v >= N).  The budget then shrinks by k cS.  A finished
+// slot keeps computing harmless garbage.
+__device__ __forceinline__ bool hs_commit(float Lf, uint32_t& cL, uint32_t cS, uint32_t& M, uint32_t k) {
+    const uint64_t P = (uint64_t)k * cS;
+    const bool done = (Lf == 0.0f) | (P >= M);
+    cL += (uint32_t)P;
+    M -= (uint32_t)P;
     return done;
 }
 
-__device__ __forceinline__ void hs_redo(uint64_t& L, uint64_t S, uint64_t& d, uint32_t& k, uint32_t k2, bool sub,
-                                        bool then_body) {
+// Undo hs_fast's in-place update (all arithmetic mod 2^64 is exact) and
+// redo the half-step with hardware division.
+__device__ __forceinline__ void hs_redo(uint64_t& L, uint64_t S, float& Lf, uint64_t& d, uint32_t& k, uint32_t k2,
+                                        bool sub, bool then_body) {
     const uint64_t L_old = L + (uint64_t)k * S;
     const uint64_t d_old = d + (uint64_t)k2 * S + (sub ? L : 0);
     const ExactStep e = hs_exact(L_old, S, d_old, then_body);
     L = e.Lp;
+    Lf = __ull2float_rn(e.Lp);
     d = e.dn;
     k = e.k;
 }
@@ -147,8 +173,7 @@ __device__ __forceinline__ void hs_redo(uint64_t& L, uint64_t S, uint64_t& d, ui
 //
 // FIRST marks the first then-half of a search (see hs_fast).
 template <bool THEN, bool FIRST = false>
-__device__ __forceinline__ void pair_step(Slot& s0, Slot& s1, uint32_t n0, uint32_t n1, bool act0, bool act1,
-                                          bool& f0, bool& f1) {
+__device__ __forceinline__ void pair_step(Slot& s0, Slot& s1, bool act0, bool act1, bool& f0, bool& f1) {
     uint64_t& L0 = THEN ? s0.A : s0.B;
     uint64_t& L1 = THEN ? s1.A : s1.B;
     const uint64_t S0 = THEN ? s0.B : s0.A, S1 = THEN ? s1.B : s1.A;
@@ -165,11 +190,11 @@ __device__ __forceinline__ void pair_step(Slot& s0, Slot& s1, uint32_t n0, uint3
     b0 = b0 && act0;
     b1 = b1 && act1;
     if (__any_sync(0xffffffffu, b0 || b1)) {
-        if (b0) hs_redo(L0, S0, s0.d, k0, q0, u0, THEN);
-        if (b1) hs_redo(L1, S1, s1.d, k1, q1, u1, THEN);
+        if (b0) hs_redo(L0, S0, Lf0, s0.d, k0, q0, u0, THEN);
+        if (b1) hs_redo(L1, S1, Lf1, s1.d, k1, q1, u1, THEN);
     }
-    f0 = hs_commit(L0, Lf0, cL0, cS0, n0, k0);
-    f1 = hs_commit(L1, Lf1, cL1, cS1, n1, k1);
+    f0 = hs_commit(Lf0, cL0, cS0, s0.M, k0);
+    f1 = hs_commit(Lf1, cL1, cS1, s1.M, k1);
 }
 
 // The lockstep loop's two building blocks.  fast_pair advances both slots
@@ -190,38 +215,40 @@ __device__ __forceinline__ bool fast_pair(Slot& s0, Slot& s1, bool act0, bool ac
 }
 
 template <bool THEN>
-__device__ __forceinline__ bool commit_slot(Slot& s, uint32_t n, uint32_t k) {
-    return THEN ? hs_commit(s.A, s.Af, s.cA, s.cB, n, k) : hs_commit(s.B, s.Bf, s.cB, s.cA, n, k);
+__device__ __forceinline__ bool commit_slot(Slot& s, uint32_t k) {
+    return THEN ? hs_commit(s.Af, s.cA, s.cB, s.M, k) : hs_commit(s.Bf, s.cB, s.cA, s.M, k);
 }
 
 // One exact half-step of parity `th` from a slot's committed state.
-__device__ __forceinline__ bool exact_half(Slot& s, bool th, uint32_t n) {
+__device__ __forceinline__ bool exact_half(Slot& s, bool th) {
     if (th) {
         const ExactStep e = hs_exact(s.A, s.B, s.d, true);
         s.A = e.Lp;
+        s.Af = __ull2float_rn(e.Lp);
         s.d = e.dn;
-        return hs_commit(s.A, s.Af, s.cA, s.cB, n, e.k);
+        return hs_commit(s.Af, s.cA, s.cB, s.M, e.k);
     }
     const ExactStep e = hs_exact(s.B, s.A, s.d, false);
     s.B = e.Lp;
+    s.Bf = __ull2float_rn(e.Lp);
     s.d = e.dn;
-    return hs_commit(s.B, s.Bf, s.cB, s.cA, n, e.k);
+    return hs_commit(s.Bf, s.cB, s.cA, s.M, e.k);
 }
 
 // Rare path: repair the half-step of parity `th` that fast_pair left
 // uncommitted (redo it exactly where it was flagged), commit it, then run
 // the slot's search to its end with exact half-steps.  Returns the
 // half-step count at the end.
-__device__ __noinline__ uint32_t slow_finish(Slot& s, bool bad, uint32_t k, uint32_t q, bool u, bool th, uint32_t h,
-                                             uint32_t n) {
+__device__ __noinline__ uint32_t slow_finish(Slot& s, bool bad, uint32_t k, uint32_t q, bool u, bool th, uint32_t h) {
     uint64_t& L = th ? s.A : s.B;
+    float& Lf = th ? s.Af : s.Bf;
     const uint64_t S = th ? s.B : s.A;
-    if (bad) hs_redo(L, S, s.d, k, q, u, th);
-    bool f = th ? hs_commit(s.A, s.Af, s.cA, s.cB, n, k) : hs_commit(s.B, s.Bf, s.cB, s.cA, n, k);
+    if (bad) hs_redo(L, S, Lf, s.d, k, q, u, th);
+    bool f = th ? hs_commit(s.Af, s.cA, s.cB, s.M, k) : hs_commit(s.Bf, s.cB, s.cA, s.M, k);
     h++;
     while (!f) {
         th = !th;
-        f = exact_half(s, th, n);
+        f = exact_half(s, th);
         h++;
     }
     return h;
@@ -254,6 +281,7 @@ __device__ __forceinline__ bool slot_init(uint64_t a, uint64_t b, uint64_t eps, 
     s.Bf = __ull2float_rn(a);
     s.cA = 1;
     s.cB = 1;
+    s.M = N - 2;  // N >= 2 here
     return false;
 }
 
@@ -275,6 +303,13 @@ __device__ __forceinline__ uint32_t lane_items(Src& src, unsigned long long* ite
     const uint32_t mine = n_items < (uint32_t)NU ? n_items : (uint32_t)NU;
     const int kend = (int)__reduce_max_sync(0xffffffffu, mine);
     Slot s0 = {}, s1 = {};
+    // a slot whose search ended after h half-steps: record its outcome
+    auto finish = [&](int item, const Slot& s, uint64_t e, uint32_t h) {
+        const uint32_t it = halve ? (h + 1) >> 1 : h;
+        its += it;
+        fails |= (s.d > e) ? 0u : 1u << item;
+        src.done(item, s.d > e, s.d, it);
+    };
 #pragma unroll 1
     for (int k = 0; k < kend; k += 2) {
         uint64_t a, b, e0 = 0, e1 = 0;
@@ -302,19 +337,13 @@ __device__ __forceinline__ uint32_t lane_items(Src& src, unsigned long long* ite
         // masked), so nothing is copied into it.
         {  // iteration 1: the then-half against one (see slot_init)
             bool f0, f1;
-            pair_step<true, true>(s0, s1, n0, n1, act0, act1, f0, f1);
-            if (act0 && f0) {
-                its += 1;
-                fails |= (s0.d > e0) ? 0u : 1u << k;
-                src.done(k, s0.d > e0, s0.d, 1);
-                act0 = false;
-            }
-            if (act1 && f1) {
-                its += 1;
-                fails |= (s1.d > e1) ? 0u : 2u << k;
-                src.done(k + 1, s1.d > e1, s1.d, 1);
-                act1 = false;
-            }
+            pair_step<true, true>(s0, s1, act0, act1, f0, f1);
+            f0 = f0 && act0;
+            f1 = f1 && act1;
+            if (f0) finish(k, s0, e0, 1);
+            if (f1) finish(k + 1, s1, e1, 1);
+            act0 = act0 && !f0;
+            act1 = act1 && !f1;
         }
         uint32_t h = 1;  // half-steps so far (both slots start after their first then-half)
         int pending = 0;  // 1 / 2: left the loop with an uncommitted else- / then-half
@@ -325,53 +354,32 @@ __device__ __forceinline__ uint32_t lane_items(Src& src, unsigned long long* ite
                 pending = 1;
                 break;
             }
-            bool f0 = commit_slot<false>(s0, n0, k0), f1 = commit_slot<false>(s1, n1, k1);
+            bool f0 = commit_slot<false>(s0, k0) && act0, f1 = commit_slot<false>(s1, k1) && act1;
             h++;
-            if (act0 && f0) {
-                its += halve ? (h + 1) >> 1 : h;
-                fails |= (s0.d > e0) ? 0u : 1u << k;
-                src.done(k, s0.d > e0, s0.d, halve ? (h + 1) >> 1 : h);
-                act0 = false;
-            }
-            if (act1 && f1) {
-                its += halve ? (h + 1) >> 1 : h;
-                fails |= (s1.d > e1) ? 0u : 2u << k;
-                src.done(k + 1, s1.d > e1, s1.d, halve ? (h + 1) >> 1 : h);
-                act1 = false;
+            if (f0 || f1) {  // one branch for both slots (rare: a search ends)
+                if (f0) finish(k, s0, e0, h);
+                if (f1) finish(k + 1, s1, e1, h);
+                act0 = act0 && !f0;
+                act1 = act1 && !f1;
             }
             if (fast_pair<true>(s0, s1, act0, act1, k0, k1, q0, q1, u0, u1, b0, b1)) {
                 pending = 2;
                 break;
             }
-            f0 = commit_slot<true>(s0, n0, k0), f1 = commit_slot<true>(s1, n1, k1);
+            f0 = commit_slot<true>(s0, k0) && act0;
+            f1 = commit_slot<true>(s1, k1) && act1;
             h++;
-            if (act0 && f0) {
-                its += halve ? (h + 1) >> 1 : h;
-                fails |= (s0.d > e0) ? 0u : 1u << k;
-                src.done(k, s0.d > e0, s0.d, halve ? (h + 1) >> 1 : h);
-                act0 = false;
-            }
-            if (act1 && f1) {
-                its += halve ? (h + 1) >> 1 : h;
-                fails |= (s1.d > e1) ? 0u : 2u << k;
-                src.done(k + 1, s1.d > e1, s1.d, halve ? (h + 1) >> 1 : h);
-                act1 = false;
+            if (f0 || f1) {
+                if (f0) finish(k, s0, e0, h);
+                if (f1) finish(k + 1, s1, e1, h);
+                act0 = act0 && !f0;
+                act1 = act1 && !f1;
             }
         }
         if (pending) {  // rare (warp-uniform entry): finish the pair's searches exactly
             const bool th = pending == 2;
-            if (act0) {
-                const uint32_t hh = slow_finish(s0, b0, k0, q0, u0, th, h, n0);
-                its += halve ? (hh + 1) >> 1 : hh;
-                fails |= (s0.d > e0) ? 0u : 1u << k;
-                src.done(k, s0.d > e0, s0.d, halve ? (hh + 1) >> 1 : hh);
-            }
-            if (act1) {
-                const uint32_t hh = slow_finish(s1, b1, k1, q1, u1, th, h, n1);
-                its += halve ? (hh + 1) >> 1 : hh;
-                fails |= (s1.d > e1) ? 0u : 2u << k;
-                src.done(k + 1, s1.d > e1, s1.d, halve ? (hh + 1) >> 1 : hh);
-            }
+            if (act0) finish(k, s0, e0, slow_finish(s0, b0, k0, q0, u0, th, h));
+            if (act1) finish(k + 1, s1, e1, slow_finish(s1, b1, k1, q1, u1, th, h));
         }
     }
     *iters += its;
