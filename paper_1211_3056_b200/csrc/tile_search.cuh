@@ -145,8 +145,14 @@ __device__ __noinline__ ExactStep hs_exact(uint64_t L, uint64_t S, uint64_t d, b
 // Lf == 0) or the count reaches N, i.e. k cS >= M = N - cL - cS (the
 // reference's u + v >= N).  The budget then shrinks by k cS.  A finished
 // slot keeps computing harmless garbage.
+__device__ __forceinline__ uint64_t mul_wide(uint32_t a, uint32_t b) {
+    uint64_t p;
+    asm("mul.wide.u32 %0, %1, %2;" : "=l"(p) : "r"(a), "r"(b));
+    return p;
+}
+
 __device__ __forceinline__ bool hs_commit(float Lf, uint32_t& cL, uint32_t cS, uint32_t& M, uint32_t k) {
-    const uint64_t P = (uint64_t)k * cS;
+    const uint64_t P = mul_wide(k, cS);
     const bool done = (Lf == 0.0f) | (P >= M);
     cL += (uint32_t)P;
     M -= (uint32_t)P;
