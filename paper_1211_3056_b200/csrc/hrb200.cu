@@ -349,6 +349,40 @@ struct WalkSrc {
         w->h0 = s1 + inc[1];
         return true;
     }
+    // items k and k + 1 with one load and one store of the walk state (the
+    // state stays in registers between the two tabulated steps)
+    __device__ __forceinline__ void build2(int k, bool& v0, uint64_t& a0, uint64_t& b0, uint64_t& e0, uint32_t& N0,
+                                           bool& v1, uint64_t& a1, uint64_t& b1, uint64_t& e1, uint32_t& N1) {
+        const uint32_t i = il + 32u * (uint32_t)k;
+        v0 = i < nd;
+        v1 = i + 32u < nd;
+        if (!v0) return;
+        const uint64_t wmask = W == 64 ? ~0ull : 0xFFFFFFFFull;
+        u128 s0 = w->g0, s1 = w->h0, g1 = w->g1;
+        const u128 g2 = inc[0], h1 = inc[1];
+        {
+            const bool last = i == nd - 1;
+            const uint64_t pad = last ? pad_last : pad_full;
+            a0 = top_bits<W, SH>(0 - s1, sh);
+            b0 = (top_bits<W, SH>(s0, sh) + pad) & wmask;
+            e0 = 2 * pad;
+            N0 = last ? nlast : nfull;
+        }
+        s0 += g1;
+        g1 += g2;
+        s1 += h1;
+        {
+            const bool last = i + 32u == nd - 1;
+            const uint64_t pad = last ? pad_last : pad_full;
+            a1 = top_bits<W, SH>(0 - s1, sh);
+            b1 = (top_bits<W, SH>(s0, sh) + pad) & wmask;
+            e1 = 2 * pad;
+            N1 = last ? nlast : nfull;
+        }
+        w->g0 = s0 + g1;
+        w->g1 = g1 + g2;
+        w->h0 = s1 + h1;
+    }
     __device__ __forceinline__ void done(int, bool, uint64_t, uint32_t) {}
 };
 
@@ -448,6 +482,11 @@ struct SubWalkSrc {
         dt0 += d2;
         t1 += dt1;
         return true;
+    }
+    __device__ __forceinline__ void build2(int k, bool& v0, uint64_t& a0, uint64_t& b0, uint64_t& e0, uint32_t& N0,
+                                           bool& v1, uint64_t& a1, uint64_t& b1, uint64_t& e1, uint32_t& N1) {
+        v0 = build(k, a0, b0, e0, N0);
+        v1 = build(k + 1, a1, b1, e1, N1);
     }
     __device__ __forceinline__ void done(int, bool, uint64_t, uint32_t) {}
 };
@@ -1031,6 +1070,11 @@ struct ArraySrc {
         ev = __ldg(&eps[i]);
         N = (uint32_t)c;
         return true;
+    }
+    __device__ __forceinline__ void build2(int k, bool& v0, uint64_t& a0, uint64_t& b0, uint64_t& e0, uint32_t& N0,
+                                           bool& v1, uint64_t& a1, uint64_t& b1, uint64_t& e1, uint32_t& N1) {
+        v0 = build(k, a0, b0, e0, N0);
+        v1 = build(k + 1, a1, b1, e1, N1);
     }
     __device__ __forceinline__ void done(int k, bool okv, uint64_t dv, uint32_t itv) {
         const int64_t i = base + 32 * (int64_t)k;

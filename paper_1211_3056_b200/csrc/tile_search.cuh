@@ -292,8 +292,8 @@ __device__ __forceinline__ bool slot_init(uint64_t a, uint64_t b, uint64_t eps, 
 }
 
 // All items of one lane, two searches at a time in lockstep.
-//   src.build(k, a, b, eps, N) builds item k; called for k = 0, 1, 2, ... in
-//   order, exactly once each; returns false for an invalid item.
+//   src.build2(k, ...) builds items k and k + 1 (k = 0, 2, 4, ... in order,
+//   exactly once each) and flags each valid or not.
 //   src.done(k, ok, d, iterations) reports each valid item's outcome (the
 //   phase kernels ignore it; the verdict batch stores it).
 // Returns the lane's failure bits (bit k = item k failed) and adds the
@@ -318,20 +318,21 @@ __device__ __forceinline__ uint32_t lane_items(Src& src, unsigned long long* ite
     };
 #pragma unroll 1
     for (int k = 0; k < kend; k += 2) {
-        uint64_t a, b, e0 = 0, e1 = 0;
+        uint64_t ia0, ib0, ia1, ib1, e0 = 0, e1 = 0;
         uint32_t n0 = 0, n1 = 0;
-        bool ok, act0 = false, act1 = false;
+        bool ok, v0, v1, act0 = false, act1 = false;
         uint64_t d_early;
-        if (src.build(k, a, b, e0, n0)) {
-            if (slot_init<W>(a, b, e0, n0, s0, &ok, &d_early)) {
+        src.build2(k, v0, ia0, ib0, e0, n0, v1, ia1, ib1, e1, n1);
+        if (v0) {
+            if (slot_init<W>(ia0, ib0, e0, n0, s0, &ok, &d_early)) {
                 fails |= ok ? 0u : 1u << k;
                 src.done(k, ok, d_early, 0);
             } else {
                 act0 = true;
             }
         }
-        if (src.build(k + 1, a, b, e1, n1)) {
-            if (slot_init<W>(a, b, e1, n1, s1, &ok, &d_early)) {
+        if (v1) {
+            if (slot_init<W>(ia1, ib1, e1, n1, s1, &ok, &d_early)) {
                 fails |= ok ? 0u : 2u << k;
                 src.done(k + 1, ok, d_early, 0);
             } else {
