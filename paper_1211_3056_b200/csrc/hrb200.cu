@@ -99,6 +99,11 @@ struct SliceDev {
     const uint32_t* last_n;
     const uint64_t* dom_base;
     const uint64_t* m0;
+    // streamed upload (hrb_run_slice_host): the coefficient rows, G and
+    // s2abs of super-domain t are valid once *ready > t / ready_chunk;
+    // nullptr when the slice is resident before the launch
+    const uint32_t* ready;
+    uint32_t ready_chunk;
 };
 
 SliceDev to_dev(const hrb_slice* s) {
@@ -116,7 +121,42 @@ SliceDev to_dev(const hrb_slice* s) {
     d.last_n = s->last_n;
     d.dom_base = s->dom_base;
     d.m0 = s->m0;
+    d.ready = nullptr;
+    d.ready_chunk = 1;
     return d;
+}
+
+// Block the warp until super-domain t's coefficients have landed (streamed
+// upload; no-op for a resident slice).  `known` is the warp's last observed
+// chunk count: tiles come in increasing order, so a warp polls about once
+// per chunk it enters.  Lane 0 polls with backoff; a counter that never gets
+// there (a host-side bug) traps after ~2 s instead of hanging the GPU.
+__device__ __forceinline__ void wait_super(const SliceDev& s, int64_t t, uint32_t& known) {
+    if (!s.ready) return;
+    const uint32_t need = (uint32_t)(t / s.ready_chunk) + 1;
+    if (need <= known) return;  // warp-uniform
+    uint32_t v = 0;
+    if ((threadIdx.x & 31) == 0) {
+        const long long t0 = clock64();
+        unsigned ns = 128;
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(s.ready) : "memory");
+        while (v < need) {
+            __nanosleep(ns);
+            ns = ns < 2048 ? 2 * ns : ns;
+            if (clock64() - t0 > 4000000000ll) __trap();
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(s.ready) : "memory");
+        }
+    }
+    known = __shfl_sync(0xffffffffu, v, 0);
+}
+
+// Loads of data that may be streamed in while the kernel runs go to L2
+// (ld.cg): a line cached in L1 before its bytes arrived would be stale.
+// Only the regular phase-1 kernel reads streamed data (CG = true).
+template <bool CG, class T>
+__device__ __forceinline__ T ld_slice(const T* p) {
+    if (CG) return __ldcg(p);
+    return __ldg(p);
 }
 
 __device__ __forceinline__ u128 mask_f(int F) { return F >= 128 ? ~(u128)0 : (((u128)1 << F) - 1); }
@@ -125,16 +165,17 @@ __device__ __forceinline__ u128 mask_f(int F) { return F >= 128 ? ~(u128)0 : (((
 // four two's-complement limbs it is just the low four limbs (the common case,
 // CL = L + 1 = 9; four loads, no shifts); narrower coefficients are
 // sign-extended
+template <bool CG = false>
 __device__ __forceinline__ u128 coef_res(const SliceDev& s, int64_t t, int c) {
     const uint32_t* base = s.coef + (int64_t)c * s.CL * s.S + t;
     if (s.CL >= 4) {
-        const uint64_t lo = (uint64_t)__ldg(base) | ((uint64_t)__ldg(base + s.S) << 32);
-        const uint64_t hi = (uint64_t)__ldg(base + 2 * s.S) | ((uint64_t)__ldg(base + 3 * s.S) << 32);
+        const uint64_t lo = (uint64_t)ld_slice<CG>(base) | ((uint64_t)ld_slice<CG>(base + s.S) << 32);
+        const uint64_t hi = (uint64_t)ld_slice<CG>(base + 2 * s.S) | ((uint64_t)ld_slice<CG>(base + 3 * s.S) << 32);
         return ((u128)hi << 64) | lo;
     }
     u128 r = 0;
-    for (int l = 0; l < s.CL; l++) r |= (u128)__ldg(base + l * s.S) << (32 * l);
-    if (__ldg(base + (s.CL - 1) * s.S) & 0x80000000u) r |= ~(u128)0 << (32 * s.CL);  // sign-extend
+    for (int l = 0; l < s.CL; l++) r |= (u128)ld_slice<CG>(base + l * s.S) << (32 * l);
+    if (ld_slice<CG>(base + (s.CL - 1) * s.S) & 0x80000000u) r |= ~(u128)0 << (32 * s.CL);  // sign-extend
     return r;
 }
 
@@ -142,6 +183,10 @@ __device__ __forceinline__ u128 coef_res(const SliceDev& s, int64_t t, int c) {
 // the pipeline's domain sizes); the 64-bit divide is a CALL to a long routine
 __device__ __forceinline__ uint64_t udiv_small(uint64_t a, uint32_t b) {
     return (a >> 32) ? a / b : (uint64_t)((uint32_t)a / b);
+}
+
+__device__ __forceinline__ u128 ld128cg(const SliceDev& s, const uint64_t* p, int64_t t) {
+    return ((u128)__ldcg(&p[s.S + t]) << 64) | __ldcg(&p[t]);
 }
 
 __device__ __forceinline__ u128 ld128(const uint64_t* p, int64_t S, int64_t t) {
@@ -405,6 +450,7 @@ __global__ void __launch_bounds__(128, HRB_P1_MINB) phase1_reg_kernel(SliceDev s
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const uint64_t total_tiles = tile_base[s.S];
     unsigned long long iters = 0;
+    uint32_t known = 0;  // streamed upload: chunks known to have landed
     WalkSrc<W, SH> src;
     src.w = &walks[threadIdx.x];
     src.inc = incs[threadIdx.x >> 5];
@@ -419,10 +465,11 @@ __global__ void __launch_bounds__(128, HRB_P1_MINB) phase1_reg_kernel(SliceDev s
 #endif
         const int64_t t = locate_super(tile_base, s.S, gw);
         const uint64_t tile = gw - tile_base[t];
-        const u128 c00 = coef_res(s, t, 0), c01 = coef_res(s, t, 1), c02 = coef_res(s, t, 2);
-        const u128 c10 = coef_res(s, t, 3), c11 = coef_res(s, t, 4);
-        const u128 G = ld128(s.G, s.S, t);
-        const u128 s2a = s.delta >= 2 ? ld128(s.s2abs, s.S, t) : (u128)0;
+        wait_super(s, t, known);
+        const u128 c00 = coef_res<true>(s, t, 0), c01 = coef_res<true>(s, t, 1), c02 = coef_res<true>(s, t, 2);
+        const u128 c10 = coef_res<true>(s, t, 3), c11 = coef_res<true>(s, t, 4);
+        const u128 G = ld128cg(s, s.G, t);
+        const u128 s2a = s.delta >= 2 ? ld128cg(s, s.s2abs, t) : (u128)0;
         src.nd = __ldg(&s.n_dom[t]);
         src.nfull = __ldg(&s.dom_n[t]);
         src.nlast = __ldg(&s.last_n[t]);
@@ -1225,8 +1272,19 @@ int run_compact(Workspace& ws, const Fn& fn, uint64_t* total, cudaStream_t st) {
     return HRB_OK;
 }
 
-int phase1_impl(Workspace& ws, const hrb_slice* s, const SliceDev& sd, int algo, int mode, uint64_t* fail_ids,
-                uint64_t* fail_count, uint64_t cap, uint64_t* iter_sum, cudaStream_t st) {
+// Streamed upload (hrb_run_slice_host): `ready` / `chunk` let the regular
+// phase-1 kernel start before the coefficients have all landed; ev_data is
+// recorded on the copy stream once every input is resident, and is waited
+// on before anything else reads them.
+struct Stream {
+    const uint32_t* ready = nullptr;
+    uint32_t chunk = 1;
+    cudaEvent_t ev_data = nullptr;
+};
+
+int phase1_impl(Workspace& ws, const hrb_slice* s, const SliceDev& sd0, int algo, int mode, uint64_t* fail_ids,
+                uint64_t* fail_count, uint64_t cap, uint64_t* iter_sum, cudaStream_t st, const Stream& up = Stream()) {
+    SliceDev sd = sd0;
     int rc;
     // upper bound of tiles: n_total/TILE + S
     const uint64_t max_tiles = (uint64_t)s->n_total / TILE + (uint64_t)s->n_super + 1;
@@ -1239,6 +1297,11 @@ int phase1_impl(Workspace& ws, const hrb_slice* s, const SliceDev& sd, int algo,
     auto tt = (uint32_t*)ws.tile_t.p;
     auto is = (unsigned long long*)iter_sum;
     auto tc = (unsigned long long*)ws.meta.p + 4;
+    if (up.ev_data && (algo < hrb::ALGO_REGULAR || !up.ready)) CK(cudaStreamWaitEvent(st, up.ev_data, 0));
+    if (algo >= hrb::ALGO_REGULAR && up.ready) {
+        sd.ready = up.ready;
+        sd.ready_chunk = up.chunk;
+    }
     if (algo >= hrb::ALGO_REGULAR) {
         const int g5 = sm_count() * HRB_P1_MINB;  // persistent: one wave at the launch bound
         if (sd.W == 64 && sd.F == 96) phase1_reg_kernel<64, 32><<<g5, 128, 0, st>>>(sd, algo, tb, bm, tt, is, tc);
@@ -1249,6 +1312,7 @@ int phase1_impl(Workspace& ws, const hrb_slice* s, const SliceDev& sd, int algo,
         else phase1_kernel<32, false><<<grid, 256, 0, st>>>(sd, algo, mode, tb, bm, tt, is);
     }
     CK(cudaGetLastError());
+    if (up.ev_data && algo >= hrb::ALGO_REGULAR && up.ready) CK(cudaStreamWaitEvent(st, up.ev_data, 0));
     P1Compact fn{(const uint32_t*)ws.bm1.p, tb, tt, s->dom_base, sd.S, fail_ids, (uint32_t*)ws.fail_t.p, cap};
     return run_compact(ws, fn, fail_count, st);
 }
@@ -1510,13 +1574,13 @@ namespace {
 // phase-1 ids and count are final, so a caller can start copying them out
 // while phases 2 and 3 run.  Caller holds g_ws_mu.
 int run_slice_locked(Workspace& ws, const hrb_slice* s, int algo, int mode, int split, const hrb_run_out* out,
-                     cudaStream_t st, cudaEvent_t ev_p1) {
+                     cudaStream_t st, cudaEvent_t ev_p1, const Stream& up = Stream()) {
     int rc;
     SliceDev sd = to_dev(s);
     uint64_t* counts = out->counts;
     CK(cudaMemsetAsync(counts, 0, sizeof(uint64_t) * 4, st));
     if ((rc = ws_prep(ws, sd, split, st))) return rc;
-    if ((rc = phase1_impl(ws, s, sd, algo, mode, out->fail_ids, counts + 0, out->fail_cap, counts + 3, st)))
+    if ((rc = phase1_impl(ws, s, sd, algo, mode, out->fail_ids, counts + 0, out->fail_cap, counts + 3, st, up)))
         return rc;
     if (ev_p1) CK(cudaEventRecord(ev_p1, st));
     if ((rc = phase2_impl(ws, s, sd, algo, mode, split, out->fail_ids, (const uint32_t*)ws.fail_t.p, counts + 0,
@@ -1602,11 +1666,14 @@ int hrb_run_slice(const hrb_slice* s, int algo, int mode, int split, const hrb_r
 }
 
 namespace {
+constexpr int UPLOAD_CHUNKS = 16;  // streamed upload: chunks of super-domains
+
 struct HostRunState {
-    Buf coef, G, s2, nd, dn, ln, db, m0, fail, sub, cm, cd, cdom, counts;
-    cudaStream_t st = nullptr, cs = nullptr;  // compute stream, copy-out stream
-    cudaEvent_t e0 = nullptr, e1 = nullptr, ep1 = nullptr;
+    Buf coef, G, s2, nd, dn, ln, db, m0, fail, sub, cm, cd, cdom, counts, ready;
+    cudaStream_t st = nullptr, cs = nullptr;  // compute stream, copy stream (uploads, id copy-out)
+    cudaEvent_t e0 = nullptr, e1 = nullptr, ep1 = nullptr, emeta = nullptr, edata = nullptr;
     uint64_t* hcount = nullptr;  // pinned scratch for the phase-1 count
+    uint32_t* hseq = nullptr;    // pinned 1 .. UPLOAD_CHUNKS: the chunk counter's values
 };
 HostRunState g_host[64];
 }  // namespace
@@ -1625,7 +1692,11 @@ int hrb_run_slice_host(const hrb_slice* hs, int algo, int mode, int split, uint6
         CK(cudaEventCreate(&H.e0));
         CK(cudaEventCreate(&H.e1));
         CK(cudaEventCreateWithFlags(&H.ep1, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&H.emeta, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&H.edata, cudaEventDisableTiming));
         CK(cudaMallocHost((void**)&H.hcount, sizeof(uint64_t)));
+        CK(cudaMallocHost((void**)&H.hseq, sizeof(uint32_t) * UPLOAD_CHUNKS));
+        for (int c = 0; c < UPLOAD_CHUNKS; c++) H.hseq[c] = (uint32_t)(c + 1);
     }
     const int64_t S = hs->n_super, CL = hs->coef_limbs, NT = hs->n_total;
     // the phases read coefficients only mod 2^128: with >= 4 two's-complement
@@ -1634,20 +1705,62 @@ int hrb_run_slice_host(const hrb_slice* hs, int algo, int mode, int split, uint6
     const size_t b_coef = sizeof(uint32_t) * 6 * CLd * S, b2 = sizeof(uint64_t) * 2 * S, b32 = sizeof(uint32_t) * S;
     if ((rc = H.coef.ensure(b_coef)) || (rc = H.G.ensure(b2)) || (rc = H.s2.ensure(b2)) || (rc = H.nd.ensure(b32)) ||
         (rc = H.dn.ensure(b32)) || (rc = H.ln.ensure(b32)) || (rc = H.db.ensure(sizeof(uint64_t) * (S + 1))) ||
-        (rc = H.m0.ensure(sizeof(uint64_t) * S)) || (rc = H.counts.ensure(sizeof(uint64_t) * 4)))
+        (rc = H.m0.ensure(sizeof(uint64_t) * S)) || (rc = H.counts.ensure(sizeof(uint64_t) * 4)) ||
+        (rc = H.ready.ensure(sizeof(uint32_t))))
         return rc;
-    cudaStream_t st = H.st;
+    cudaStream_t st = H.st, cs = H.cs;
+    // Upload on the copy stream.  The per-super-domain sizes and offsets go
+    // first (prep and phase 1's tile walk need them before the launch).  For
+    // the regular family the rest is streamed: coefficients, G, s2abs and m0
+    // in runs of super-domains, each followed by a 4-byte write of its
+    // sequence number to a chunk counter that phase 1's warps wait on
+    // (wait_super).  The compute sequence is enqueued after the first run, so
+    // the upload of the others overlaps the search; phase 1 reads every
+    // super-domain, so whatever follows it finds the slice resident.  The
+    // classic family (no wait in its kernel) uploads everything first.
+    const bool stream_in = algo >= hrb::ALGO_REGULAR;
     CK(cudaEventRecord(H.e0, st));
-    for (int c = 0; c < 6; c++)  // rows c*CL .. c*CL + CLd - 1 are contiguous in the host layout
-        CK(cudaMemcpyAsync((uint32_t*)H.coef.p + (int64_t)c * CLd * S, hs->coef + (int64_t)c * CL * S,
-                           sizeof(uint32_t) * CLd * S, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(H.G.p, hs->G, b2, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(H.s2.p, hs->s2abs, b2, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(H.nd.p, hs->n_dom, b32, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(H.dn.p, hs->dom_n, b32, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(H.ln.p, hs->last_n, b32, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(H.db.p, hs->dom_base, sizeof(uint64_t) * (S + 1), cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(H.m0.p, hs->m0, sizeof(uint64_t) * S, cudaMemcpyHostToDevice, st));
+    CK(cudaStreamWaitEvent(cs, H.e0, 0));  // nothing of the previous call still reads the buffers
+    CK(cudaMemsetAsync(H.ready.p, 0, sizeof(uint32_t), cs));
+    CK(cudaMemcpyAsync(H.nd.p, hs->n_dom, b32, cudaMemcpyHostToDevice, cs));
+    CK(cudaMemcpyAsync(H.dn.p, hs->dom_n, b32, cudaMemcpyHostToDevice, cs));
+    CK(cudaMemcpyAsync(H.ln.p, hs->last_n, b32, cudaMemcpyHostToDevice, cs));
+    CK(cudaMemcpyAsync(H.db.p, hs->dom_base, sizeof(uint64_t) * (S + 1), cudaMemcpyHostToDevice, cs));
+    const int64_t nchunk = !stream_in ? 1 : (S < UPLOAD_CHUNKS ? S : UPLOAD_CHUNKS);
+    const int64_t per = (S + nchunk - 1) / nchunk;
+    auto upload_chunk = [&](int64_t c) -> int {
+        const int64_t t0 = c * per, n = (t0 + per <= S ? per : S - t0);
+        cudaMemcpy3DParms p = {};
+        // 6 coefficients x CLd limb rows of n words; host rows have pitch S
+        // words and CL rows per coefficient, device rows CLd
+        p.srcPtr = make_cudaPitchedPtr((void*)(hs->coef + t0), sizeof(uint32_t) * S, sizeof(uint32_t) * n, CL);
+        p.dstPtr = make_cudaPitchedPtr((uint32_t*)H.coef.p + t0, sizeof(uint32_t) * S, sizeof(uint32_t) * n, CLd);
+        p.extent = make_cudaExtent(sizeof(uint32_t) * n, CLd, 6);
+        p.kind = cudaMemcpyHostToDevice;
+        CK(cudaMemcpy3DAsync(&p, cs));
+        CK(cudaMemcpy2DAsync((uint64_t*)H.G.p + t0, sizeof(uint64_t) * S, hs->G + t0, sizeof(uint64_t) * S,
+                             sizeof(uint64_t) * n, 2, cudaMemcpyHostToDevice, cs));
+        CK(cudaMemcpy2DAsync((uint64_t*)H.s2.p + t0, sizeof(uint64_t) * S, hs->s2abs + t0, sizeof(uint64_t) * S,
+                             sizeof(uint64_t) * n, 2, cudaMemcpyHostToDevice, cs));
+        CK(cudaMemcpyAsync((uint64_t*)H.m0.p + t0, hs->m0 + t0, sizeof(uint64_t) * n, cudaMemcpyHostToDevice, cs));
+        if (stream_in)
+            CK(cudaMemcpyAsync(H.ready.p, H.hseq + c, sizeof(uint32_t), cudaMemcpyHostToDevice, cs));
+        return HRB_OK;
+    };
+    if (!stream_in) {
+        if ((rc = upload_chunk(0))) return rc;
+        CK(cudaEventRecord(H.edata, cs));
+        CK(cudaStreamWaitEvent(st, H.edata, 0));
+    } else {
+        CK(cudaEventRecord(H.emeta, cs));
+        if ((rc = upload_chunk(0))) return rc;
+        CK(cudaStreamWaitEvent(st, H.emeta, 0));
+    }
+    Stream up;
+    if (stream_in) {
+        up.ready = (const uint32_t*)H.ready.p;
+        up.chunk = (uint32_t)per;
+    }
     hrb_slice ds = *hs;
     ds.coef = (const uint32_t*)H.coef.p;
     ds.coef_limbs = (int32_t)CLd;
@@ -1683,8 +1796,13 @@ int hrb_run_slice_host(const hrb_slice* hs, int algo, int mode, int split, uint6
             if ((rc = current_ws(&ws))) return rc;
             if ((rc = check_slice(&ds)) || (rc = check_algo(algo, mode))) return rc;
             if (split < 2 || split > 64) return set_err(HRB_ERR_CONFIG, "phase2_split outside {2..64}");
-            if ((rc = run_slice_locked(*ws, &ds, algo, mode, split, &o, st, fail_copied ? nullptr : H.ep1))) return rc;
+            if ((rc = run_slice_locked(*ws, &ds, algo, mode, split, &o, st, fail_copied ? nullptr : H.ep1,
+                                       attempt == 0 ? up : Stream())))
+                return rc;
         }
+        if (attempt == 0 && stream_in)  // the rest of the upload, behind the launched search
+            for (int64_t c = 1; c * per < S; c++)
+                if ((rc = upload_chunk(c))) return rc;
         if (!fail_copied) {
             // the failing ids are final after phase 1: copy them out on the
             // copy stream while phases 2 and 3 run on the compute stream

@@ -114,7 +114,10 @@ def test_tabulated_values_match_reference(name):
             assert v == int(hx, 16), (name, k, j)
 
 
-@pytest.mark.parametrize("name", ["p53_exp_2p20_e16_N12", "p53_exp_ragged", "p13_log_b0"])
+# p13_log_b0 (41 super-domains) and p16_exp_b1 (131) stream their upload in
+# 16 chunks through hrb_run_slice_host; the Lefevre cases upload up front
+@pytest.mark.parametrize("name", ["p53_exp_2p20_e16_N12", "p53_exp_ragged", "p13_log_b0", "p16_exp_b1",
+                                  "p53_exp_delta1", "p13_exp_b0_lefevre", "p53_exp_lef_hw"])
 def test_fused_and_host_paths_equal_phase_path(name):
     from paper_1211_3056_b200.device import DeviceSlice, FusedRunner, run_host, run_phases
 
