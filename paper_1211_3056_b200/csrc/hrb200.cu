@@ -1131,20 +1131,23 @@ struct ArraySrc {
     }
 };
 
-template <int W>
+// NUV problems per lane: the phases' NU for large batches; small batches
+// (config 2's 2^17 problems) take 2 per lane so that they still fill the GPU
+template <int W, int NUV>
 __global__ void __launch_bounds__(128, HRB_P1_MINB) search_verdict_kernel(int algo, int64_t n, const uint64_t* a,
                                                                           const uint64_t* b, const uint64_t* eps,
                                                                           const uint64_t* count, uint8_t* ok,
                                                                           uint64_t* d, uint64_t* it) {
+    constexpr int TV = 32 * NUV;
     const int lane = threadIdx.x & 31;
     const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    const int64_t tiles = (n + TILE - 1) / TILE;
+    const int64_t tiles = (n + TV - 1) / TV;
     ArraySrc<W> src{a, b, eps, count, ok, d, it, n, 0, algo == hrb::ALGO_REGULAR_UNROLLED};
     for (int64_t t = warp0; t < tiles; t += nwarps) {
-        src.base = t * TILE + lane;
+        src.base = t * TV + lane;
         unsigned long long its = 0;
-        hrb::lane_items<W, NU>(src, &its, src.unrolled);
+        hrb::lane_items<W, NUV>(src, &its, src.unrolled);
     }
 }
 
@@ -1462,14 +1465,18 @@ int hrb_search_verdicts(int algo, int word_bits, int64_t n, const uint64_t* a, c
     if (n < 0) return set_err(HRB_ERR_CONFIG, "negative batch size");
     if (n == 0) return HRB_OK;
     cudaStream_t st = (cudaStream_t)stream;
-    const int64_t tiles = (n + TILE - 1) / TILE;
-    const int64_t blocks = (tiles * 32 + 127) / 128;
     const int64_t cap = (int64_t)sm_count() * HRB_P1_MINB;
+    const bool small = n < cap * 4 * 32 * NU;  // fewer tiles of 32 NU than 4 per resident warp
+    const int64_t tv = 32 * (small ? 2 : NU);
+    const int64_t blocks = ((n + tv - 1) / tv * 32 + 127) / 128;
     const int grid = (int)(blocks < cap ? blocks : cap);
-    if (word_bits == 64)
-        search_verdict_kernel<64><<<grid, 128, 0, st>>>(algo, n, a, b, eps, count, ok, d, iterations);
-    else
-        search_verdict_kernel<32><<<grid, 128, 0, st>>>(algo, n, a, b, eps, count, ok, d, iterations);
+#define LAUNCH(WV, NV) search_verdict_kernel<WV, NV><<<grid, 128, 0, st>>>(algo, n, a, b, eps, count, ok, d, iterations)
+    if (word_bits == 64) {
+        if (small) LAUNCH(64, 2); else LAUNCH(64, NU);
+    } else {
+        if (small) LAUNCH(32, 2); else LAUNCH(32, NU);
+    }
+#undef LAUNCH
     CK(cudaGetLastError());
     return HRB_OK;
 }
