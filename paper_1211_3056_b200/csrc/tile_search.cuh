@@ -20,6 +20,7 @@
 
 #include "search_core.cuh"
 
+
 namespace hrb {
 
 // One search in flight.  The reference's (p, q) pair lives in two fixed
@@ -109,7 +110,11 @@ __device__ __forceinline__ void hs_fast(uint64_t& L, uint64_t S, float& Lf, floa
     const uint32_t ke2 = (uint32_t)max(qfloor(__ull2float_rn(x), rcp), 0);
     const uint64_t y = madd64(x, ke2, nS);
     const float rf = __ull2float_rn(r);
-    bad = (ke >= QMAX) | !(rf < Sf) | (y >= S);
+    // 0 < r < S, proved in float by one product: (rf - Sf) rf < 0 exactly
+    // when 0 < rf < Sf (rf = 0, rf >= Sf and an overflow to +inf all fail
+    // it).  r == 0 -- the expansion exhausted, rare before the count limit --
+    // is left to the exact path, whose commit ends the search.
+    bad = (ke >= QMAX) | !(__fmul_rn(rf - Sf, rf) < 0.0f) | (y >= S);
     if (FIRST) bad |= (r > L) | (y > x);
     // in place: the old L and d are recoverable from (r, y, ke, ke2, sub)
     // on the exact path, so no copy of them stays live across the vote
@@ -151,9 +156,11 @@ __device__ __forceinline__ uint64_t mul_wide(uint32_t a, uint32_t b) {
     return p;
 }
 
+template <bool ZERO = true>
 __device__ __forceinline__ bool hs_commit(float Lf, uint32_t& cL, uint32_t cS, uint32_t& M, uint32_t k) {
     const uint64_t P = mul_wide(k, cS);
-    const bool done = (Lf == 0.0f) | (P >= M);
+    // ZERO = false: the fast loop's commit, where r == 0 was flagged bad
+    const bool done = (ZERO && Lf == 0.0f) | (P >= M);
     cL += (uint32_t)P;
     M -= (uint32_t)P;
     return done;
@@ -222,7 +229,7 @@ __device__ __forceinline__ bool fast_pair(Slot& s0, Slot& s1, bool act0, bool ac
 
 template <bool THEN>
 __device__ __forceinline__ bool commit_slot(Slot& s, uint32_t k) {
-    return THEN ? hs_commit(s.Af, s.cA, s.cB, s.M, k) : hs_commit(s.Bf, s.cB, s.cA, s.M, k);
+    return THEN ? hs_commit<false>(s.Af, s.cA, s.cB, s.M, k) : hs_commit<false>(s.Bf, s.cB, s.cA, s.M, k);
 }
 
 // One exact half-step of parity `th` from a slot's committed state.
