@@ -1673,7 +1673,10 @@ int hrb_run_slice(const hrb_slice* s, int algo, int mode, int split, const hrb_r
 }
 
 namespace {
-constexpr int UPLOAD_CHUNKS = 16;  // streamed upload: chunks of super-domains
+#ifndef HRB_UPLOAD_CHUNKS
+#define HRB_UPLOAD_CHUNKS 8
+#endif
+constexpr int UPLOAD_CHUNKS = HRB_UPLOAD_CHUNKS;  // streamed upload: runs of super-domains
 
 struct HostRunState {
     Buf coef, G, s2, nd, dn, ln, db, m0, fail, sub, cm, cd, cdom, counts, ready;
@@ -1721,10 +1724,12 @@ int hrb_run_slice_host(const hrb_slice* hs, int algo, int mode, int split, uint6
     // the regular family the rest is streamed: coefficients, G, s2abs and m0
     // in runs of super-domains, each followed by a 4-byte write of its
     // sequence number to a chunk counter that phase 1's warps wait on
-    // (wait_super).  The compute sequence is enqueued after the first run, so
-    // the upload of the others overlaps the search; phase 1 reads every
-    // super-domain, so whatever follows it finds the slice resident.  The
-    // classic family (no wait in its kernel) uploads everything first.
+    // (wait_super), so the upload overlaps the search; phase 1 reads every
+    // super-domain, so whatever follows it finds the slice resident.  Every
+    // copy is enqueued before the search: a workspace allocation inside the
+    // run (cudaFree synchronises the device) must never wait on a kernel that
+    // waits on a copy not yet issued.  The classic family (no wait in its
+    // kernel) uploads everything before the search starts.
     const bool stream_in = algo >= hrb::ALGO_REGULAR;
     CK(cudaEventRecord(H.e0, st));
     CK(cudaStreamWaitEvent(cs, H.e0, 0));  // nothing of the previous call still reads the buffers
@@ -1760,7 +1765,8 @@ int hrb_run_slice_host(const hrb_slice* hs, int algo, int mode, int split, uint6
         CK(cudaStreamWaitEvent(st, H.edata, 0));
     } else {
         CK(cudaEventRecord(H.emeta, cs));
-        if ((rc = upload_chunk(0))) return rc;
+        for (int64_t c = 0; c * per < S; c++)
+            if ((rc = upload_chunk(c))) return rc;
         CK(cudaStreamWaitEvent(st, H.emeta, 0));
     }
     Stream up;
@@ -1807,9 +1813,6 @@ int hrb_run_slice_host(const hrb_slice* hs, int algo, int mode, int split, uint6
                                        attempt == 0 ? up : Stream())))
                 return rc;
         }
-        if (attempt == 0 && stream_in)  // the rest of the upload, behind the launched search
-            for (int64_t c = 1; c * per < S; c++)
-                if ((rc = upload_chunk(c))) return rc;
         if (!fail_copied) {
             // the failing ids are final after phase 1: copy them out on the
             // copy stream while phases 2 and 3 run on the compute stream
