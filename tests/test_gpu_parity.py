@@ -393,3 +393,29 @@ def test_run_range_intervals_equal_one_slice_and_switch_algorithms():
     for k in range(1, len(out2.choices)):
         ratio = out2.interval_stats[k - 1].phase3_phase1_ratio()
         assert out2.choices[k][1] == ("lefevre" if ratio > 1e-3 else "regular")
+
+
+def test_host_path_first_call_in_fresh_process():
+    """hrb_run_slice_host as the first call of a process (unsized workspace:
+    its allocations happen while the streamed upload is in flight) must
+    neither deadlock nor differ from the phase path."""
+    import subprocess
+    import sys
+
+    code = (
+        "import numpy as np\n"
+        "from golden_io import batch_of, case\n"
+        "from paper_1211_3056_b200.device import DeviceSlice, run_host, run_phases\n"
+        "c = case('p16_exp_b1')\n"
+        "b = batch_of(c)\n"
+        "counts, fail, cm, cd, cdom, ms = run_host(b, 2, 1, c['cfg']['split'])\n"
+        "ref = run_phases(DeviceSlice(b), 2, 1, c['cfg']['split'])\n"
+        "assert np.array_equal(fail, ref.fail_ids) and np.array_equal(cm, ref.cand_index)\n"
+        "assert np.array_equal(cd, ref.cand_dist) and np.array_equal(cdom, ref.cand_dom)\n"
+        "print('ok')\n")
+    import os
+
+    env = dict(os.environ, PYTHONPATH=os.pathsep.join([os.path.dirname(__file__), os.path.dirname(os.path.dirname(
+        os.path.abspath(__file__))), os.environ.get("PYTHONPATH", "")]))
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300, env=env)
+    assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-2000:]
