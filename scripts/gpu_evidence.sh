@@ -29,3 +29,6 @@ cat gpurun_out/bench_$T.json
 HRB_BENCH_ONE_DEVICE=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 \
   --master-port 29531 bench.py --gpus 2 --steps 3 --warmup 3 --log2-args 36 --no-e2e > gpurun_out/multirank2_$T.json 2> gpurun_out/multirank2_$T.err
 echo "multirank rc=$?"
+# where the end-to-end call's time goes (fresh process: unsized workspace)
+timeout 300 python scripts/e2e_probe.py > gpurun_out/e2e_probe_$T.log 2>&1
+tail -n 1 gpurun_out/e2e_probe_$T.log
