@@ -97,9 +97,16 @@ def main():
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / a.reps
             iters = it.cpu().numpy().view(np.uint64)
-            out["algos"][name] = {"kernel_ms": ms, "args_per_s": args_total / (ms / 1e3),
-                                  "quotient_steps_per_s": float(iters.sum()) / (ms / 1e3),
-                                  "it_mean": float(iters.mean()), "mean_nmdm": warp_summary(iters).mean_nmdm}
+            rec = {"kernel_ms": ms, "args_per_s": args_total / (ms / 1e3),
+                   "quotient_steps_per_s": float(iters.sum()) / (ms / 1e3),
+                   "it_mean": float(iters.mean()), "mean_nmdm": warp_summary(iters).mean_nmdm}
+            if not a.no_cpu:  # (verdict, d, iterations) against the oracle, as for the general forms
+                base = "regular" if code == 2 else "regular_unrolled"
+                wok, wd, wit, _, _ = oracle.search_batch(base, 1, 1 << 64, A, B, E, N)
+                rec["bit_exact_vs_oracle"] = bool(np.array_equal(wit, iters)
+                                                  and np.array_equal(wd, d.cpu().numpy().view(np.uint64))
+                                                  and np.array_equal(wok, ok.cpu().numpy()))
+            out["algos"][name] = rec
     print(json.dumps(out), flush=True)
 
 
