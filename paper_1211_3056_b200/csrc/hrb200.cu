@@ -64,12 +64,6 @@ int cuda_err(cudaError_t e, const char* where) {
 #ifndef HRB_P2_MINB
 #define HRB_P2_MINB 5
 #endif
-#ifndef HRB_P1_DYN
-#define HRB_P1_DYN 1  // phase-1 regular kernel: dynamic tile scheduler
-#endif
-#ifndef HRB_P2_DYN
-#define HRB_P2_DYN 1  // phase-2 regular kernel: dynamic chunk scheduler
-#endif
 #ifndef HRB_NU
 #define HRB_NU 16
 #endif
@@ -455,14 +449,10 @@ __global__ void __launch_bounds__(128, HRB_P1_MINB) phase1_reg_kernel(SliceDev s
     src.w = &walks[threadIdx.x];
     src.inc = incs[threadIdx.x >> 5];
     src.sh = 128 - s.F;
-#if HRB_P1_DYN
     uint64_t gw = warp0;
     while (gw < total_tiles) {
         unsigned long long next = 0;
         if (lane == 0) next = nwarps + atomicAdd(tile_ctr, 1ull);
-#else
-    for (uint64_t gw = warp0; gw < total_tiles; gw += nwarps) {
-#endif
         const int64_t t = locate_super(tile_base, s.S, gw);
         const uint64_t tile = gw - tile_base[t];
         wait_super(s, t, known);
@@ -497,9 +487,7 @@ __global__ void __launch_bounds__(128, HRB_P1_MINB) phase1_reg_kernel(SliceDev s
         }
         if (lane < NU) bitmap[gw * NU + lane] = mine;
         if (lane == 0) tile_t[gw] = (uint32_t)t;
-#if HRB_P1_DYN
         gw = __shfl_sync(0xffffffffu, next, 0);
-#endif
     }
     for (int o = 16; o > 0; o >>= 1) iters += __shfl_xor_sync(0xffffffffu, iters, o);
     if (iter_sum && lane == 0 && iters) atomicAdd(iter_sum, iters);
@@ -551,7 +539,6 @@ __global__ void __launch_bounds__(128, HRB_P2_MINB) phase2_reg_kernel(SliceDev s
     src.sh = 128 - s.F;
     // whole warps iterate together so the lockstep pairs stay converged
     const uint64_t nf_pad = (nf + 31) & ~31ull;
-#if HRB_P2_DYN
     // a warp takes 32 consecutive failing domains at a time, the first chunk
     // by its id and the rest from a device counter (meta[5], zeroed by
     // ws_prep), fetched one chunk ahead (see phase1_reg_kernel)
@@ -562,10 +549,6 @@ __global__ void __launch_bounds__(128, HRB_P2_MINB) phase2_reg_kernel(SliceDev s
         unsigned long long next = 0;
         if (lane == 0) next = nwarps + atomicAdd(&meta[5], 1ull);
         const uint64_t f = 32 * chunk + lane;
-#else
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t f = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; f < nf_pad; f += stride) {
-#endif
         const bool valid = f < nf;
         src.nsub = 0;
         if (valid) {
@@ -600,9 +583,7 @@ __global__ void __launch_bounds__(128, HRB_P2_MINB) phase2_reg_kernel(SliceDev s
             const uint32_t fails = hrb::lane_items<W, 32>(src, &its, false, src.nsub > 32 * c ? src.nsub - 32 * c : 0);
             if (valid) bitmap[f * wpd + c] = fails;
         }
-#if HRB_P2_DYN
         chunk = __shfl_sync(0xffffffffu, next, 0);
-#endif
     }
 }
 
@@ -1338,11 +1319,7 @@ int phase2_impl(Workspace& ws, const hrb_slice* s, const SliceDev& sd, int algo,
     auto mt = (unsigned long long*)ws.meta.p;
     auto bm = (uint32_t*)ws.bm2.p;
     if (algo >= hrb::ALGO_REGULAR) {
-#if HRB_P2_DYN
         const int g4 = sm_count() * HRB_P2_MINB;  // persistent: one wave, chunks from the counter
-#else
-        const int g4 = sm_count() * HRB_P2_MINB * 4;  // grid-stride over failing domains (device count)
-#endif
         if (sd.W == 64 && sd.F == 96)
             phase2_reg_kernel<64, 32><<<g4, 128, 0, st>>>(sd, split, fail_ids, fail_t, fail_count, fail_cap, mt, bm);
         else if (sd.W == 64)
