@@ -432,7 +432,7 @@ struct WalkSrc {
 // repairs; a static grid-stride split left ~17 % of the warp slots idle at
 // the end of the kernel.  The bitmap and tile_t are indexed by tile, so the
 // output does not depend on which warp ran which tile.
-template <int W, int SH>
+template <int W, int SH, int PL>
 __global__ void __launch_bounds__(128, HRB_P1_MINB) phase1_reg_kernel(SliceDev s, int algo, const uint64_t* tile_base,
                                                           uint32_t* bitmap, uint32_t* tile_t,
                                                           unsigned long long* iter_sum,
@@ -442,17 +442,22 @@ __global__ void __launch_bounds__(128, HRB_P1_MINB) phase1_reg_kernel(SliceDev s
     const int lane = threadIdx.x & 31;
     const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    const uint64_t total_tiles = tile_base[s.S];
+    // work unit: a tile, or a quarter of one (PL = 2) for slices with too
+    // few tiles to keep every warp busy to the end
+    const uint64_t units = tile_base[s.S] << PL;
+    constexpr uint32_t nper = (uint32_t)NU >> PL;
     unsigned long long iters = 0;
     uint32_t known = 0;  // streamed upload: chunks known to have landed
     WalkSrc<W, SH> src;
     src.w = &walks[threadIdx.x];
     src.inc = incs[threadIdx.x >> 5];
     src.sh = 128 - s.F;
-    uint64_t gw = warp0;
-    while (gw < total_tiles) {
+    uint64_t u = warp0;
+    while (u < units) {
         unsigned long long next = 0;
         if (lane == 0) next = nwarps + atomicAdd(tile_ctr, 1ull);
+        const uint64_t gw = u >> PL;
+        const uint32_t k0 = (uint32_t)(u & ((1u << PL) - 1)) * nper;  // first item of the part
         const int64_t t = locate_super(tile_base, s.S, gw);
         const uint64_t tile = gw - tile_base[t];
         wait_super(s, t, known);
@@ -465,7 +470,7 @@ __global__ void __launch_bounds__(128, HRB_P1_MINB) phase1_reg_kernel(SliceDev s
         src.nlast = __ldg(&s.last_n[t]);
         src.pad_full = pad_of(G, s2a, src.nfull, s.F, W);
         src.pad_last = pad_of(G, s2a, src.nlast, s.F, W);
-        const uint64_t il = tile * TILE + lane;
+        const uint64_t il = tile * TILE + 32 * k0 + lane;
         src.il = (uint32_t)il;
         __syncwarp();
         src.w->g0 = c00 + c01 * (u128)il + c02 * (u128)binom2(il);
@@ -477,7 +482,7 @@ __global__ void __launch_bounds__(128, HRB_P1_MINB) phase1_reg_kernel(SliceDev s
         }
         __syncwarp();
         unsigned long long its = 0;
-        const uint32_t fails = hrb::lane_items<W, NU>(src, &its, algo == hrb::ALGO_REGULAR_UNROLLED);
+        const uint32_t fails = hrb::lane_items<W, NU>(src, &its, algo == hrb::ALGO_REGULAR_UNROLLED, nper);
         iters += its;
         uint32_t mine = 0;
 #pragma unroll
@@ -485,9 +490,9 @@ __global__ void __launch_bounds__(128, HRB_P1_MINB) phase1_reg_kernel(SliceDev s
             uint32_t wd = __ballot_sync(0xffffffffu, (fails >> k) & 1u);
             if (lane == k) mine = wd;
         }
-        if (lane < NU) bitmap[gw * NU + lane] = mine;
+        if (lane < nper) bitmap[gw * NU + k0 + lane] = mine;
         if (lane == 0) tile_t[gw] = (uint32_t)t;
-        gw = __shfl_sync(0xffffffffu, next, 0);
+        u = __shfl_sync(0xffffffffu, next, 0);
     }
     for (int o = 16; o > 0; o >>= 1) iters += __shfl_xor_sync(0xffffffffu, iters, o);
     if (iter_sum && lane == 0 && iters) atomicAdd(iter_sum, iters);
@@ -1288,9 +1293,19 @@ int phase1_impl(Workspace& ws, const hrb_slice* s, const SliceDev& sd0, int algo
     }
     if (algo >= hrb::ALGO_REGULAR) {
         const int g5 = sm_count() * HRB_P1_MINB;  // persistent: one wave at the launch bound
-        if (sd.W == 64 && sd.F == 96) phase1_reg_kernel<64, 32><<<g5, 128, 0, st>>>(sd, algo, tb, bm, tt, is, tc);
-        else if (sd.W == 64) phase1_reg_kernel<64, -1><<<g5, 128, 0, st>>>(sd, algo, tb, bm, tt, is, tc);
-        else phase1_reg_kernel<32, -1><<<g5, 128, 0, st>>>(sd, algo, tb, bm, tt, is, tc);
+        // quarter tiles when there are fewer than ~8 tiles per resident warp
+        // (the last round of 512-domain tiles would idle most of the GPU);
+        // the bitmap layout does not change
+        const bool quarter = (uint64_t)s->n_total / TILE + 1 < (uint64_t)g5 * 4 * 8;
+#define P1(WV, SHV, PLV) phase1_reg_kernel<WV, SHV, PLV><<<g5, 128, 0, st>>>(sd, algo, tb, bm, tt, is, tc)
+        if (sd.W == 64 && sd.F == 96) {
+            if (quarter) P1(64, 32, 2); else P1(64, 32, 0);
+        } else if (sd.W == 64) {
+            if (quarter) P1(64, -1, 2); else P1(64, -1, 0);
+        } else {
+            if (quarter) P1(32, -1, 2); else P1(32, -1, 0);
+        }
+#undef P1
     } else {
         if (sd.W == 64) phase1_kernel<64, false><<<grid, 256, 0, st>>>(sd, algo, mode, tb, bm, tt, is);
         else phase1_kernel<32, false><<<grid, 256, 0, st>>>(sd, algo, mode, tb, bm, tt, is);
