@@ -86,7 +86,7 @@ def prepare_rank(args, rank, world, workers):
     blocks = plan_blocks(args.fn, 0, cfg.fmt, cfg.polygen, args.start, world << args.log2_args)
     b0, b1 = partition_blocks([b.bcount for b in blocks], world)[rank]
     supers = supers_of_blocks(blocks[b0:b1], workers)
-    batch = pack_slice(supers, cfg.fmt, cfg.polygen, cfg.word_bits, 0)
+    batch = pack_slice(supers, cfg.fmt, cfg.polygen, cfg.word_bits, 0, workers=workers)
     return batch, time.perf_counter() - t0
 
 

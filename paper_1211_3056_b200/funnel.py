@@ -231,7 +231,7 @@ def prepare_slice(fn: str, binade: int, start: int, count: int, cfg: PipelineCon
     w = workers if workers is not None else cfg.phase.parallel_width
     supers = build_super_domains(fn, binade, cfg.fmt, cfg.polygen, start, count, workers=w, id0=id0)
     ceiling = cfg.phase.budgets.eps_dprime if cfg.phase.budgets is not None else None
-    return pack_slice(supers, cfg.fmt, cfg.polygen, cfg.word_bits, binade, budget_ceiling=ceiling)
+    return pack_slice(supers, cfg.fmt, cfg.polygen, cfg.word_bits, binade, budget_ceiling=ceiling, workers=w)
 
 
 def run_slice(fn: str, binade: int, start: int, count: int, cfg: PipelineConfig, algo: str | None = None,
@@ -286,7 +286,7 @@ def run_range(fn: str, binade: int, start: int, count: int, cfg: PipelineConfig,
 
     def prepare(part):
         supers = supers_of_blocks(blocks[part[0]:part[1]], w)
-        return pack_slice(supers, cfg.fmt, cfg.polygen, cfg.word_bits, binade, budget_ceiling=ceiling)
+        return pack_slice(supers, cfg.fmt, cfg.polygen, cfg.word_bits, binade, budget_ceiling=ceiling, workers=w)
 
     records, stats_list, choices = [], [], []
     prev = None

@@ -141,7 +141,7 @@ def _run_rank(blocks, rank, world, fn, binade, cfg, algo, workers, confirm) -> S
         return ShardResult(np.zeros(N_COUNTERS, np.int64))
     supers = supers_of_blocks(mine, workers)
     ceiling = cfg.phase.budgets.eps_dprime if cfg.phase.budgets is not None else None
-    batch = pack_slice(supers, cfg.fmt, cfg.polygen, cfg.word_bits, binade, budget_ceiling=ceiling)
+    batch = pack_slice(supers, cfg.fmt, cfg.polygen, cfg.word_bits, binade, budget_ceiling=ceiling, workers=workers)
     out = execute_batch(batch, cfg, _resolve(cfg, algo), fn, confirm=confirm)
     return ShardResult.of(len(out.failing_ids), len(out.sub_rows), out.candidates, out.records,
                           out.iterations, batch.arguments)

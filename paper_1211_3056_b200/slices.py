@@ -317,22 +317,17 @@ def _limbs_of(v: int, cl: int) -> list[int]:
 COEF_SLOTS = ((0, 0), (0, 1), (0, 2), (1, 0), (1, 1), (2, 0))  # (j, l) of coef rows
 
 
-def pack_slice(supers: Sequence[SuperDomain], fmt: FpFormat, pg: PolyGenConfig, word_bits: int,
-               binade: int, budget_ceiling: Fraction | None = None, check: bool = True) -> SliceBatch:
-    if not supers:
-        raise ValueError("empty slice")
+def _pack_rows(supers: Sequence[SuperDomain], fmt: FpFormat, pg: PolyGenConfig, word_bits: int,
+               budget_ceiling: Fraction | None, check: bool):
+    """The packed columns of a run of super-domains (and their checks, which
+    raise exactly where the reference would)."""
     F = pg.frac_bits
-    if not word_bits <= F <= 128:
-        raise ValueError(f"the B200 path needs word_bits <= frac_bits <= 128 (got F={F}, W={word_bits})")
     S = len(supers)
     cl = pg.limbs + 1  # MPInt magnitude < 2^(32 L) fits L+1 two's complement limbs
     coef = np.zeros((6, cl, S), dtype=np.uint32)
     G = np.zeros((2, S), dtype=np.uint64)
     s2 = np.zeros((2, S), dtype=np.uint64)
-    n_dom = np.zeros(S, dtype=np.uint32)
-    dom_n = np.zeros(S, dtype=np.uint32)
-    last_n = np.zeros(S, dtype=np.uint32)
-    m0 = np.zeros(S, dtype=np.uint64)
+    meta = np.zeros((4, S), dtype=np.uint64)  # n_dom, dom_n, last_n, m0
     ok2 = np.ones(S, dtype=bool)
     m128 = (1 << 64) - 1
     for t, sd in enumerate(supers):
@@ -346,8 +341,49 @@ def pack_slice(supers: Sequence[SuperDomain], fmt: FpFormat, pg: PolyGenConfig, 
         if len(sd.r_polys) > 2:
             a = min(abs(as_int(sd.r_polys[2].coeffs[0])), (1 << 128) - 1)
             s2[0, t], s2[1, t] = a & m128, a >> 64
-        n_dom[t], dom_n[t], last_n[t] = sd.tau, sd.n_p, sd.last_count
-        m0[t] = sd.index_start
+        meta[:, t] = (sd.tau, sd.n_p, sd.last_count, sd.index_start)
+    return coef, G, s2, meta, ok2
+
+
+_PACK_JOB = None  # (supers, fmt, pg, word_bits, ceiling, check): inherited by forked workers
+
+
+def _pack_range(rng):
+    supers, fmt, pg, word_bits, ceiling, check = _PACK_JOB
+    return _pack_rows(supers[rng[0]:rng[1]], fmt, pg, word_bits, ceiling, check)
+
+
+def pack_slice(supers: Sequence[SuperDomain], fmt: FpFormat, pg: PolyGenConfig, word_bits: int,
+               binade: int, budget_ceiling: Fraction | None = None, check: bool = True,
+               workers: int = 1) -> SliceBatch:
+    """hrb_slice columns of the super-domains, after the host checks.
+    workers > 1 packs runs of super-domains in forked processes (the exact
+    Fraction / MPInt checks dominate at 2^16 super-domains); a check that
+    fails raises the error of the first failing super-domain, as the
+    sequential loop does."""
+    global _PACK_JOB
+    if not supers:
+        raise ValueError("empty slice")
+    F = pg.frac_bits
+    if not word_bits <= F <= 128:
+        raise ValueError(f"the B200 path needs word_bits <= frac_bits <= 128 (got F={F}, W={word_bits})")
+    S = len(supers)
+    if workers > 1 and S >= 4 * workers:
+        import multiprocessing as mp
+
+        per = -(-S // (4 * workers))
+        ranges = [(a, min(a + per, S)) for a in range(0, S, per)]
+        _PACK_JOB = (list(supers), fmt, pg, word_bits, budget_ceiling, check)
+        try:
+            with mp.get_context("fork").Pool(workers) as pool:
+                parts = pool.map(_pack_range, ranges, chunksize=1)
+        finally:
+            _PACK_JOB = None
+        coef, G, s2, meta, ok2 = (np.concatenate([p[k] for p in parts], axis=-1) for k in range(5))
+    else:
+        coef, G, s2, meta, ok2 = _pack_rows(supers, fmt, pg, word_bits, budget_ceiling, check)
+    n_dom, dom_n, last_n = (meta[k].astype(np.uint32) for k in range(3))
+    m0 = meta[3].copy()
     dom_base = np.zeros(S + 1, dtype=np.uint64)
     np.cumsum(n_dom, out=dom_base[1:])
     return SliceBatch(list(supers), fmt, binade, F, word_bits, pg.delta, pg.limbs, coef, G, s2, n_dom, dom_n,

@@ -53,3 +53,22 @@ def test_confirmation_matches_reference_records(workers, monkeypatch):
         cand = [HrCaseRecord(int(h, 16), UFrac(d, 64), i) for h, d, i in c["phase3"]]
         recs = funnel.confirm_candidates(c["fn"], cand, cfg.fmt, workers)
         assert essence(recs) == c["records"], name
+
+
+def test_parallel_packing_is_identical():
+    """pack_slice over forked workers equals the sequential packing, column
+    for column, and a failing host check still raises."""
+    import numpy as np
+
+    from paper_1211_3056_b200.slices import pack_slice
+
+    c = case("p16_exp_b1")  # 131 super-domains
+    cfg = config_of(c)
+    sup = build_super_domains(c["fn"], c["binade"], cfg.fmt, cfg.polygen, *c["slice"])
+    a = pack_slice(sup, cfg.fmt, cfg.polygen, cfg.word_bits, c["binade"])
+    b = pack_slice(sup, cfg.fmt, cfg.polygen, cfg.word_bits, c["binade"], workers=4)
+    for k in ("coef", "G", "s2abs", "n_dom", "dom_n", "last_n", "dom_base", "m0", "shift_bound_ok"):
+        x, y = getattr(a, k), getattr(b, k)
+        assert x.dtype == y.dtype and np.array_equal(x, y), k
+    with pytest.raises(ValueError):
+        pack_slice(sup, cfg.fmt, cfg.polygen, cfg.word_bits, c["binade"], budget_ceiling=Fraction(0), workers=4)
