@@ -189,7 +189,13 @@ int hrb_run_slice(const hrb_slice* s, int algo, int mode, int split, const hrb_r
  * back, synchronises.  Host outputs: counts[4], fail_ids (<= fail_cap),
  * cand_* (<= cand_cap).  Device buffers are cached per device and grown on
  * demand (a too-small internal subdomain buffer triggers one re-run).
- * device_ms (may be NULL) receives the kernel-only time of the last run.
+ * For the regular family the upload is streamed behind the search (phase 1
+ * waits per run of super-domains on a device counter) and the failing ids
+ * are copied back while phases 2-3 run.  One call at a time per device: the
+ * cached buffers and streams are per device, not per thread.
+ * device_ms (may be NULL) receives the time between the call's first and
+ * last event on its compute stream (uploads overlapped, final copies
+ * included).
  */
 int hrb_run_slice_host(const hrb_slice* host_slice, int algo, int mode, int split,
                        uint64_t* counts, uint64_t* fail_ids, uint64_t fail_cap,
