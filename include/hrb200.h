@@ -191,8 +191,8 @@ int hrb_run_slice(const hrb_slice* s, int algo, int mode, int split, const hrb_r
  * demand (a too-small internal subdomain buffer triggers one re-run).
  * For the regular family the upload is streamed behind the search (phase 1
  * waits per run of super-domains on a device counter) and the failing ids
- * are copied back while phases 2-3 run.  One call at a time per device: the
- * cached buffers and streams are per device, not per thread.
+ * are copied back while phases 2-3 run.  Calls on the same device are
+ * serialised (the cached buffers and streams are per device).
  * device_ms (may be NULL) receives the time between the call's first and
  * last event on its compute stream (uploads overlapped, final copies
  * included).

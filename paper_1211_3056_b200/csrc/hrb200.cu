@@ -1678,6 +1678,7 @@ struct HostRunState {
     uint32_t* hseq = nullptr;    // pinned 1 .. UPLOAD_CHUNKS: the chunk counter's values
 };
 HostRunState g_host[64];
+std::mutex g_host_mu[64];  // one host-buffer call at a time per device (shared buffers, streams)
 }  // namespace
 
 int hrb_run_slice_host(const hrb_slice* hs, int algo, int mode, int split, uint64_t* counts, uint64_t* fail_ids,
@@ -1687,6 +1688,7 @@ int hrb_run_slice_host(const hrb_slice* hs, int algo, int mode, int split, uint6
     if (rc || (rc = check_algo(algo, mode))) return rc;
     int dev = 0;
     CK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> host_lk(g_host_mu[dev & 63]);
     HostRunState& H = g_host[dev & 63];
     if (!H.st) {
         CK(cudaStreamCreateWithFlags(&H.st, cudaStreamNonBlocking));
