@@ -97,7 +97,10 @@ def workload_name(args):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """Clocks and throttle reasons sampled during the timed region.  NVML
+    (the library nvidia-smi reads) is polled every ~0.5 ms, so even a 20 ms
+    region gets dozens of in-region samples; without pynvml, nvidia-smi is
+    run in a loop instead."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -105,20 +108,53 @@ class ClockSampler:
     def __init__(self, index: int):
         self.index = index
         self.samples = []
+        self.source = "nvidia-smi"
         self._stop = threading.Event()
         self._t = None
+        self._nvml = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nvml = (pynvml, pynvml.nvmlDeviceGetHandleByIndex(index))
+            self.source = "nvml"
+        except Exception:
+            self._nvml = None
+
+    def _sample_nvml(self):
+        nv, h = self._nvml
+        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        flags = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                 nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+        return [str(sm), str(mx)] + ["Active" if r & f else "Not Active" for f in flags]
 
     def _run(self):
         while not self._stop.is_set():
             try:
+                if self._nvml is not None:
+                    self.samples.append(self._sample_nvml())
+                    time.sleep(0.0005)
+                    continue
                 out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
                                       "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
                 vals = [v.strip() for v in out.stdout.strip().split(",")]
                 if len(vals) == 6:
                     self.samples.append(vals)
             except Exception:
-                pass
+                self._nvml = None  # fall back to nvidia-smi
             self._stop.wait(0.05)
+
+    def sample_now(self):
+        """One NVML sample from the calling thread (the timed loop calls it
+        between step launches: the GPU is then running queued steps, and the
+        per-step CUDA events do not see host time)."""
+        if self._nvml is not None:
+            try:
+                self.samples.append(self._sample_nvml())
+            except Exception:
+                pass
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -137,7 +173,7 @@ class ClockSampler:
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
         reasons = sorted({names[k] for s in self.samples for k in range(4) if s[2 + k].lower() == "active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+                "reasons": reasons, "samples": len(self.samples), "source": self.source}
 
 
 def load_calibration():
@@ -315,6 +351,7 @@ def main():
             evs[k][0].record(stream)
             runner.launch()
             evs[k][1].record(stream)
+            sampler.sample_now()
         torch.cuda.synchronize()
     if dist:
         dist.barrier()
