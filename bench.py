@@ -200,6 +200,7 @@ def cpu_baseline(args, batch, min_seconds):
     import oracle
 
     oracle.build()
+    oracle.set_threads(os.cpu_count() or 1)
     times, counts = [], None
     t_end = time.perf_counter() + min_seconds
     while not times or time.perf_counter() < t_end:
@@ -222,6 +223,7 @@ def run_reference(args):
 
     oracle.build()
     workers = os.cpu_count() or 1
+    oracle.set_threads(workers)  # all host threads, whatever OMP_NUM_THREADS torchrun exported
     batch, _ = prepare_rank(args, 0, 1, workers)
     times = []
     for k in range(args.warmup + args.steps):
