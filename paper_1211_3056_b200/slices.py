@@ -346,6 +346,7 @@ def _pack_rows(supers: Sequence[SuperDomain], fmt: FpFormat, pg: PolyGenConfig, 
 
 
 _PACK_JOB = None  # (supers, fmt, pg, word_bits, ceiling, check): inherited by forked workers
+PACK_PARALLEL_MIN = 1024  # super-domains below which packing stays in-process (a fork costs more)
 
 
 def _pack_range(rng):
@@ -368,7 +369,7 @@ def pack_slice(supers: Sequence[SuperDomain], fmt: FpFormat, pg: PolyGenConfig, 
     if not word_bits <= F <= 128:
         raise ValueError(f"the B200 path needs word_bits <= frac_bits <= 128 (got F={F}, W={word_bits})")
     S = len(supers)
-    if workers > 1 and S >= 4 * workers:
+    if workers > 1 and S >= max(4 * workers, PACK_PARALLEL_MIN):
         import multiprocessing as mp
 
         per = -(-S // (4 * workers))

@@ -55,12 +55,15 @@ def test_confirmation_matches_reference_records(workers, monkeypatch):
         assert essence(recs) == c["records"], name
 
 
-def test_parallel_packing_is_identical():
+def test_parallel_packing_is_identical(monkeypatch):
     """pack_slice over forked workers equals the sequential packing, column
     for column, and a failing host check still raises."""
     import numpy as np
 
+    from paper_1211_3056_b200 import slices
     from paper_1211_3056_b200.slices import pack_slice
+
+    monkeypatch.setattr(slices, "PACK_PARALLEL_MIN", 0)
 
     c = case("p16_exp_b1")  # 131 super-domains
     cfg = config_of(c)
