@@ -261,8 +261,67 @@ class RangeOutput:
     choices: list  # (first argument index, algorithm) per interval
 
 
+# ------------------------------------------------ resumable range manifest
+#
+# A JSON-lines file: a header naming the run (a hash of everything that
+# determines its results), then one line per finished interval with its
+# records, phase stats and algorithm.  run_range(manifest=path) appends a line
+# (flushed and fsynced) after every interval and, when the file already
+# exists, restores the finished intervals instead of recomputing them: a long
+# range resumes at interval granularity after a crash (SURVEY.md 2,
+# checkpoint / resume).  A line torn by a crash is ignored.
+
+
+def manifest_key(fn: str, binade: int, start: int, count: int, cfg: PipelineConfig, interval_args: int,
+                 confirm: bool = True) -> str:
+    import hashlib
+
+    return hashlib.sha256(repr((fn, binade, start, count, cfg, interval_args, confirm)).encode()).hexdigest()[:32]
+
+
+def interval_line(k: int, bstart: int, algo: str, records, stats: PhaseStats) -> str:
+    import json
+
+    return json.dumps({"kind": "interval", "k": k, "bstart": bstart, "algo": algo,
+                       "records": [[hex(r.argument), r.distance.raw, r.distance.width, r.domain_id, r.undecided]
+                                   for r in records],
+                       "rows": [[r.phase, r.domains_in, r.domains_out, r.arguments_covered, r.wall_ms]
+                                for r in stats.rows],
+                       "choices": [list(c) for c in stats.algorithm_choices]})
+
+
+def read_manifest(path: str, key: str) -> dict:
+    """Finished intervals of a manifest: {k: (bstart, algo, records, stats)}.
+    Raises ValueError when the file belongs to a different run."""
+    import json
+    import os
+
+    done = {}
+    if not os.path.exists(path):
+        return done
+    with open(path) as fh:
+        lines = fh.read().splitlines()
+    header = False
+    for line in lines:
+        try:
+            d = json.loads(line)
+        except ValueError:
+            continue  # a line torn by a crash
+        if d.get("kind") == "header":
+            if d.get("key") != key:
+                raise ValueError(f"manifest {path} belongs to another run (key {d.get('key')} != {key})")
+            header = True
+            continue
+        if not header:
+            raise ValueError(f"manifest {path} has no header")
+        recs = [HrCaseRecord(int(a, 16), UFrac(raw, width), dom, bool(und)) for a, raw, width, dom, und in d["records"]]
+        st = PhaseStats([PhaseRow(*r) for r in d["rows"]], [tuple(c) for c in d["choices"]])
+        done[int(d["k"])] = (int(d["bstart"]), d["algo"], recs, st)
+    return done
+
+
 def run_range(fn: str, binade: int, start: int, count: int, cfg: PipelineConfig, interval_args: int = 1 << 36,
-              workers: int | None = None, confirm: bool = True) -> RangeOutput:
+              workers: int | None = None, confirm: bool = True, manifest: str | None = None) -> RangeOutput:
     """A long argument range as consecutive intervals, the way the paper walks
     a binade: the block schedule of the WHOLE range is
     planned once (so blocks, domain ids and results are exactly those of a
@@ -271,7 +330,8 @@ def run_range(fn: str, binade: int, start: int, count: int, cfg: PipelineConfig,
     chosen from the previous interval's funnel (select_algorithm,
     pipeline.py:187-197).  The host Taylor generation of interval i+1 runs in
     a background thread while the device and the host confirmation work on
-    interval i."""
+    interval i.  manifest: a path that makes the run resumable (see
+    read_manifest); finished intervals are restored, not recomputed."""
     from concurrent.futures import ThreadPoolExecutor
 
     from .shard import partition_blocks
@@ -288,22 +348,59 @@ def run_range(fn: str, binade: int, start: int, count: int, cfg: PipelineConfig,
         supers = supers_of_blocks(blocks[part[0]:part[1]], w)
         return pack_slice(supers, cfg.fmt, cfg.polygen, cfg.word_bits, binade, budget_ceiling=ceiling, workers=w)
 
+    done, sink = {}, None
+    if manifest is not None:
+        import json
+        import os
+
+        key = manifest_key(fn, binade, start, count, cfg, interval_args, confirm)
+        done = read_manifest(manifest, key)
+        fresh = not os.path.exists(manifest) or os.path.getsize(manifest) == 0
+        if not fresh:
+            with open(manifest, "rb") as fh:
+                fh.seek(-1, os.SEEK_END)
+                torn = fh.read(1) != b"\n"
+        sink = open(manifest, "a")
+        if not fresh and torn:
+            sink.write("\n")  # end a line torn by a crash; read_manifest skips it
+        if fresh:
+            sink.write(json.dumps({"kind": "header", "key": key, "fn": fn, "binade": binade, "start": start,
+                                   "count": count, "intervals": len(parts)}) + "\n")
+            sink.flush()
+    todo = [k for k in range(len(parts)) if k not in done]
     records, stats_list, choices = [], [], []
     prev = None
-    with ThreadPoolExecutor(max_workers=1) as ex:
-        nxt = ex.submit(prepare, parts[0]) if parts else None
-        for k, part in enumerate(parts):
-            batch = nxt.result()
-            nxt = ex.submit(prepare, parts[k + 1]) if k + 1 < len(parts) else None
-            algo = cfg.phase.algorithm
-            if algo == "auto":
-                algo = select_algorithm(prev)
-            out = execute_batch(batch, cfg, algo, fn, confirm=confirm)
-            out.stats.algorithm_choices.append((blocks[part[0]].bstart, algo))
-            records.extend(out.records)
-            stats_list.append(out.stats)
-            choices.append((blocks[part[0]].bstart, algo))
-            prev = out.stats
+    try:
+        with ThreadPoolExecutor(max_workers=1) as ex:
+            futs = {todo[0]: ex.submit(prepare, parts[todo[0]])} if todo else {}
+            for k, part in enumerate(parts):
+                if k in done:  # restored from the manifest
+                    bstart, algo, recs, st = done[k]
+                    records.extend(recs)
+                    stats_list.append(st)
+                    choices.append((bstart, algo))
+                    prev = st
+                    continue
+                batch = futs.pop(k).result()
+                i = todo.index(k)
+                if i + 1 < len(todo):
+                    futs[todo[i + 1]] = ex.submit(prepare, parts[todo[i + 1]])
+                algo = cfg.phase.algorithm
+                if algo == "auto":
+                    algo = select_algorithm(prev)
+                out = execute_batch(batch, cfg, algo, fn, confirm=confirm)
+                out.stats.algorithm_choices.append((blocks[part[0]].bstart, algo))
+                records.extend(out.records)
+                stats_list.append(out.stats)
+                choices.append((blocks[part[0]].bstart, algo))
+                prev = out.stats
+                if sink is not None:
+                    sink.write(interval_line(k, blocks[part[0]].bstart, algo, out.records, out.stats) + "\n")
+                    sink.flush()
+                    os.fsync(sink.fileno())
+    finally:
+        if sink is not None:
+            sink.close()
     records.sort()
     return RangeOutput(records, stats_list, choices)
 
