@@ -61,9 +61,10 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--minutes", type=float, default=10.0)
     ap.add_argument("--batch", type=int, default=1 << 20)
+    ap.add_argument("--seed", type=int, default=20261017)
     a_ = ap.parse_args()
     oracle.build()
-    rng = np.random.default_rng(20261017)
+    rng = np.random.default_rng(a_.seed)
     t0 = time.time()
     stats = {"lockstep_problems": 0, "general_problems": 0, "mismatches": 0, "batches": 0}
     bad = []
