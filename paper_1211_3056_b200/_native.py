@@ -109,11 +109,11 @@ def load(path: str | None = None):
     with _lock:
         if _lib is not None:
             return _lib
-        path = path or os.environ.get("HRB_LIB") or LIB
-        if not os.path.exists(path):
+        path = path or os.environ.get("HRB_LIB")
+        if path is None:
             from .build import build
 
-            build()
+            path = build()  # recompiles only when the sources' content hash changed
         lib = C.CDLL(path)
         _declare(lib)
         _lib = lib

@@ -40,11 +40,23 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found: the CUDA toolkit is required to build libhrb200.so")
 
 
+def source_hash(sources: list) -> str:
+    """Content hash of a library's sources, headers and flags (mtimes do not
+    survive copies of the tree, e.g. the snapshot sent to a GPU box)."""
+    import hashlib
+
+    h = hashlib.sha256(" ".join(NVCC_FLAGS).encode())
+    for p in sorted(sources + HEADERS):
+        with open(p, "rb") as fh:
+            h.update(os.path.basename(p).encode() + b"\0" + fh.read())
+    return h.hexdigest()[:32]
+
+
 def _stale(lib: str, sources: list) -> bool:
-    if not os.path.exists(lib):
+    if not os.path.exists(lib) or not os.path.exists(lib + ".srchash"):
         return True
-    t = os.path.getmtime(lib)
-    return any(os.path.getmtime(p) > t for p in sources + HEADERS)
+    with open(lib + ".srchash") as fh:
+        return fh.read().strip() != source_hash(sources)
 
 
 def _compile(lib: str, sources: list, verbose: bool) -> None:
@@ -58,6 +70,9 @@ def _compile(lib: str, sources: list, verbose: bool) -> None:
     if verbose:
         sys.stderr.write(proc.stderr)
     os.replace(tmp, lib)
+    with open(lib + ".srchash.tmp", "w") as fh:
+        fh.write(source_hash(sources))
+    os.replace(lib + ".srchash.tmp", lib + ".srchash")
 
 
 def build(force: bool = False, verbose: bool = False) -> str:

@@ -123,8 +123,10 @@ SliceDev to_dev(const hrb_slice* s) {
 // Block the warp until super-domain t's coefficients have landed (streamed
 // upload; no-op for a resident slice).  `known` is the warp's last observed
 // chunk count: tiles come in increasing order, so a warp polls about once
-// per chunk it enters.  Lane 0 polls with backoff; a counter that never gets
-// there (a host-side bug) traps after ~2 s instead of hanging the GPU.
+// per chunk it enters.  Lane 0 polls with backoff.  A counter that never
+// gets there (a lost copy, a host-side bug) is given up on after ~60 s of SM
+// clock: the warp raises ready[1] (the host turns it into HRB_ERR_RUNTIME)
+// and proceeds, so one failed call never kills the CUDA context.
 __device__ __forceinline__ void wait_super(const SliceDev& s, int64_t t, uint32_t& known) {
     if (!s.ready) return;
     const uint32_t need = (uint32_t)(t / s.ready_chunk) + 1;
@@ -137,11 +139,19 @@ __device__ __forceinline__ void wait_super(const SliceDev& s, int64_t t, uint32_
         while (v < need) {
             __nanosleep(ns);
             ns = ns < 2048 ? 2 * ns : ns;
-            if (clock64() - t0 > 4000000000ll) __trap();
+            if (clock64() - t0 > 120000000000ll) {
+                atomicExch(const_cast<uint32_t*>(s.ready) + 1, 1u);
+                v = need;
+                break;
+            }
             asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(s.ready) : "memory");
         }
     }
     known = __shfl_sync(0xffffffffu, v, 0);
+    // order every lane's later ld.cg after lane 0's acquire (a shuffle
+    // carries the value, not the memory ordering; __syncwarp orders memory
+    // among the warp's threads)
+    __syncwarp();
 }
 
 // Loads of data that may be streamed in while the kernel runs go to L2
@@ -1676,6 +1686,7 @@ struct HostRunState {
     cudaEvent_t e0 = nullptr, e1 = nullptr, ep1 = nullptr, emeta = nullptr, edata = nullptr;
     uint64_t* hcount = nullptr;  // pinned scratch for the phase-1 count
     uint32_t* hseq = nullptr;    // pinned 1 .. UPLOAD_CHUNKS: the chunk counter's values
+    uint32_t* hflag = nullptr;   // pinned: wait_super timeout flag read back after a streamed call
 };
 HostRunState g_host[64];
 std::mutex g_host_mu[64];  // one host-buffer call at a time per device (shared buffers, streams)
@@ -1700,6 +1711,7 @@ int hrb_run_slice_host(const hrb_slice* hs, int algo, int mode, int split, uint6
         CK(cudaEventCreateWithFlags(&H.edata, cudaEventDisableTiming));
         CK(cudaMallocHost((void**)&H.hcount, sizeof(uint64_t)));
         CK(cudaMallocHost((void**)&H.hseq, sizeof(uint32_t) * UPLOAD_CHUNKS));
+        CK(cudaMallocHost((void**)&H.hflag, sizeof(uint32_t)));
         for (int c = 0; c < UPLOAD_CHUNKS; c++) H.hseq[c] = (uint32_t)(c + 1);
     }
     const int64_t S = hs->n_super, CL = hs->coef_limbs, NT = hs->n_total;
@@ -1710,7 +1722,7 @@ int hrb_run_slice_host(const hrb_slice* hs, int algo, int mode, int split, uint6
     if ((rc = H.coef.ensure(b_coef)) || (rc = H.G.ensure(b2)) || (rc = H.s2.ensure(b2)) || (rc = H.nd.ensure(b32)) ||
         (rc = H.dn.ensure(b32)) || (rc = H.ln.ensure(b32)) || (rc = H.db.ensure(sizeof(uint64_t) * (S + 1))) ||
         (rc = H.m0.ensure(sizeof(uint64_t) * S)) || (rc = H.counts.ensure(sizeof(uint64_t) * 4)) ||
-        (rc = H.ready.ensure(sizeof(uint32_t))))
+        (rc = H.ready.ensure(2 * sizeof(uint32_t))))
         return rc;
     cudaStream_t st = H.st, cs = H.cs;
     // Upload on the copy stream.  The per-super-domain sizes and offsets go
@@ -1727,7 +1739,7 @@ int hrb_run_slice_host(const hrb_slice* hs, int algo, int mode, int split, uint6
     const bool stream_in = algo >= hrb::ALGO_REGULAR;
     CK(cudaEventRecord(H.e0, st));
     CK(cudaStreamWaitEvent(cs, H.e0, 0));  // nothing of the previous call still reads the buffers
-    CK(cudaMemsetAsync(H.ready.p, 0, sizeof(uint32_t), cs));
+    CK(cudaMemsetAsync(H.ready.p, 0, 2 * sizeof(uint32_t), cs));  // chunk counter, timeout flag
     CK(cudaMemcpyAsync(H.nd.p, hs->n_dom, b32, cudaMemcpyHostToDevice, cs));
     CK(cudaMemcpyAsync(H.dn.p, hs->dom_n, b32, cudaMemcpyHostToDevice, cs));
     CK(cudaMemcpyAsync(H.ln.p, hs->last_n, b32, cudaMemcpyHostToDevice, cs));
@@ -1833,8 +1845,10 @@ int hrb_run_slice_host(const hrb_slice* hs, int algo, int mode, int split, uint6
     }
     CK(cudaStreamSynchronize(H.cs));
     CK(cudaEventRecord(H.e1, st));
+    if (stream_in) CK(cudaMemcpyAsync(H.hflag, (uint32_t*)H.ready.p + 1, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     if (device_ms) CK(cudaEventElapsedTime(device_ms, H.e0, H.e1));
+    if (stream_in && *H.hflag) return set_err(HRB_ERR_RUNTIME, "streamed upload never arrived (wait_super timed out)");
     if (counts[0] > fail_cap && fail_ids) return set_err(HRB_ERR_CAPACITY, "fail_ids buffer too small");
     if (counts[2] > cand_cap) return set_err(HRB_ERR_CAPACITY, "candidate buffer too small");
     return HRB_OK;

@@ -272,11 +272,20 @@ class RangeOutput:
 # checkpoint / resume).  A line torn by a crash is ignored.
 
 
+MANIFEST_VERSION = 2  # bump when the interval-line format or the results of a config change
+
+
 def manifest_key(fn: str, binade: int, start: int, count: int, cfg: PipelineConfig, interval_args: int,
                  confirm: bool = True) -> str:
+    """Hash of everything that determines a run's results.  The host worker
+    count (PhaseConfig.parallel_width) does not change results, so it is
+    normalised out: a run may resume on a machine with other core counts."""
+    import dataclasses
     import hashlib
 
-    return hashlib.sha256(repr((fn, binade, start, count, cfg, interval_args, confirm)).encode()).hexdigest()[:32]
+    norm = dataclasses.replace(cfg, phase=dataclasses.replace(cfg.phase, parallel_width=1))
+    ident = (MANIFEST_VERSION, fn, binade, start, count, norm, interval_args, confirm)
+    return hashlib.sha256(repr(ident).encode()).hexdigest()[:32]
 
 
 def interval_line(k: int, bstart: int, algo: str, records, stats: PhaseStats) -> str:
@@ -290,14 +299,30 @@ def interval_line(k: int, bstart: int, algo: str, records, stats: PhaseStats) ->
                        "choices": [list(c) for c in stats.algorithm_choices]})
 
 
+def _manifest_has_header(path: str) -> bool:
+    import json
+    import os
+
+    if not os.path.exists(path):
+        return False
+    with open(path) as fh:
+        for line in fh:
+            try:
+                return json.loads(line).get("kind") == "header"
+            except ValueError:
+                return False  # the header itself was torn by a crash
+    return False
+
+
 def read_manifest(path: str, key: str) -> dict:
     """Finished intervals of a manifest: {k: (bstart, algo, records, stats)}.
-    Raises ValueError when the file belongs to a different run."""
+    Raises ValueError when the file belongs to a different run.  A file
+    without a valid header (a crash tore it) holds no finished interval."""
     import json
     import os
 
     done = {}
-    if not os.path.exists(path):
+    if not os.path.exists(path) or not _manifest_has_header(path):
         return done
     with open(path) as fh:
         lines = fh.read().splitlines()
@@ -355,18 +380,23 @@ def run_range(fn: str, binade: int, start: int, count: int, cfg: PipelineConfig,
 
         key = manifest_key(fn, binade, start, count, cfg, interval_args, confirm)
         done = read_manifest(manifest, key)
-        fresh = not os.path.exists(manifest) or os.path.getsize(manifest) == 0
+        # no valid header (absent, empty, or torn by a crash before its
+        # newline was durable): start the file over
+        fresh = not _manifest_has_header(manifest)
+        torn = False
         if not fresh:
             with open(manifest, "rb") as fh:
                 fh.seek(-1, os.SEEK_END)
                 torn = fh.read(1) != b"\n"
-        sink = open(manifest, "a")
-        if not fresh and torn:
+        sink = open(manifest, "w" if fresh else "a")
+        if torn:
             sink.write("\n")  # end a line torn by a crash; read_manifest skips it
         if fresh:
-            sink.write(json.dumps({"kind": "header", "key": key, "fn": fn, "binade": binade, "start": start,
-                                   "count": count, "intervals": len(parts)}) + "\n")
+            sink.write(json.dumps({"kind": "header", "key": key, "version": MANIFEST_VERSION, "fn": fn,
+                                   "binade": binade, "start": start, "count": count,
+                                   "intervals": len(parts)}) + "\n")
             sink.flush()
+            os.fsync(sink.fileno())
     todo = [k for k in range(len(parts)) if k not in done]
     records, stats_list, choices = [], [], []
     prev = None
