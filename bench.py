@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="minimum CPU-baseline timing window")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-e2e-full", action="store_true", help="skip the run_range end-to-end measurement")
     return ap.parse_args()
 
 
@@ -77,17 +78,51 @@ def make_cfg(args):
 
 
 def prepare_rank(args, rank, world, workers):
-    """The rank's contiguous share of [0, world 2^log2_args), packed."""
+    """The rank's contiguous share of [0, world 2^log2_args), planned and
+    packed (native host generation where it covers the configuration)."""
     from paper_1211_3056_b200.shard import partition_blocks
-    from paper_1211_3056_b200.slices import pack_slice, plan_blocks, supers_of_blocks
+    from paper_1211_3056_b200.slices import pack_plan, plan_arrays
 
     cfg = make_cfg(args)
     t0 = time.perf_counter()
-    blocks = plan_blocks(args.fn, 0, cfg.fmt, cfg.polygen, args.start, world << args.log2_args)
-    b0, b1 = partition_blocks([b.bcount for b in blocks], world)[rank]
-    supers = supers_of_blocks(blocks[b0:b1], workers)
-    batch = pack_slice(supers, cfg.fmt, cfg.polygen, cfg.word_bits, 0, workers=workers)
+    plan = plan_arrays(args.fn, 0, cfg.fmt, cfg.polygen, args.start, world << args.log2_args)
+    b0, b1 = partition_blocks(plan.sizes, world)[rank]
+    batch = pack_plan(plan[b0:b1], cfg.word_bits, workers=workers)
     return batch, time.perf_counter() - t0
+
+
+def e2e_full(args, batch, workers, dist):
+    """funnel.run_range over the rank's whole range, as a user calls it: block
+    planning, host Taylor generation (native), packing, upload, phases 1-3,
+    download, rigorous confirmation of the candidates; wall clock, after one
+    untimed run (library loads, allocator warm-up)."""
+    import torch
+
+    from paper_1211_3056_b200.funnel import run_range
+
+    cfg = make_cfg(args)
+    start, count = int(batch.m0[0]), batch.arguments
+    interval = 1 << min(args.log2_args, 38)
+    run = lambda: run_range(args.fn, 0, start, count, cfg, interval_args=interval, workers=workers)  # noqa: E731
+    out = run()
+    ts = []
+    for _ in range(3):
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        out = run()
+        torch.cuda.synchronize()
+        ts.append(time.perf_counter() - t0)
+    rows = {}
+    for st in out.interval_stats:
+        for r in st.rows:
+            rows[r.phase] = rows.get(r.phase, 0.0) + r.wall_ms
+    return {"seconds": float(np.median(ts)), "records": len(out.records), "intervals": len(out.interval_stats),
+            "interval_args": interval, "workers": workers,
+            "phase_wall_ms": {k: round(v, 3) for k, v in rows.items()},
+            "host_generation": "native (libhrbhost.so)" if batch.supers.__class__.__name__ == "PackedSupers"
+            else "python (mpmath)"}
 
 
 def workload_name(args):
@@ -374,10 +409,13 @@ def main():
             t0 = time.perf_counter()
             hc, hf, hm, hd, hdom = host.run()
             e2e_t.append(time.perf_counter() - t0)
-        assert np.array_equal(hc, counts), "host-buffer path disagrees with the device path"
+        assert np.array_equal(hc[:4], counts), "host-buffer path disagrees with the device path"
         e2e_ms = 1e3 * float(np.mean(e2e_t))
         e2e = {"value": None, "unit": UNIT, "h2d_bytes_per_step": host.input_bytes(),
                "d2h_bytes_per_step": host.output_bytes(), "ms_per_step": e2e_ms}
+    full = None
+    if not args.no_e2e_full:
+        full = e2e_full(args, batch, workers, dist)
     # ---- end of run: NCCL gather of the per-rank counters and candidate lists
     from paper_1211_3056_b200.fpformat import index_bits
     from paper_1211_3056_b200.shard import ShardResult, gather_shards
@@ -388,8 +426,8 @@ def main():
                      for b, d, i in zip(bits, res.cand_dist.tolist(), res.cand_dom.tolist())],
                     dtype=np.uint64).reshape(-1, 4)
     local_res = ShardResult(np.array([counts[0], counts[1], counts[2], 0, counts[3], count], dtype=np.int64), cand)
-    t_all = torch.tensor([ms, float(np.median(p1_ms)), e2e["ms_per_step"] if e2e else 0.0],
-                         device="cpu" if one_dev else "cuda")
+    t_all = torch.tensor([ms, float(np.median(p1_ms)), e2e["ms_per_step"] if e2e else 0.0,
+                          full["seconds"] if full else 0.0], device="cpu" if one_dev else "cuda")
     gather_ms = 0.0
     if dist:
         dist.all_reduce(t_all, op=dist.ReduceOp.MAX)
@@ -399,7 +437,7 @@ def main():
         gather_ms = 1e3 * (time.perf_counter() - tg)
     else:
         merged, per_rank = local_res, local_res.counters[None, :]
-    ms_max, p1_max, e2e_max = (float(x) for x in t_all.cpu())
+    ms_max, p1_max, e2e_max, full_max = (float(x) for x in t_all.cpu())
     if rank != 0:
         dist.destroy_process_group()
         return
@@ -408,6 +446,10 @@ def main():
     if e2e:
         e2e["value"] = total_args / (e2e_max / 1e3)
         e2e["ms_per_step"] = e2e_max
+    if full:
+        full["seconds"] = full_max
+        full["value"] = total_args / full_max
+        full["unit"] = UNIT
     clocks = sampler.summary()
     # ---- roofline of the dominant kernel (phase 1): INT-pipe bound
     peak = int_peak()
@@ -449,7 +491,8 @@ def main():
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u64",
-            "data": f"synthetic: {args.fn} binade [1,2) argument ranges, Taylor blocks generated on the host (mpmath)",
+            "data": f"synthetic: {args.fn} binade [1,2) argument ranges, Taylor blocks generated on the host "
+                    f"({'native, bit-identical to mpmath' if batch.supers.__class__.__name__ == 'PackedSupers' else 'mpmath'})",
             "config": {"workload": workload_name(args),
                        "parallelism": f"shard{world} (contiguous super-domain blocks, no collective on the hot path; "
                                       f"NCCL gather of counters + candidates at the end)",
@@ -460,7 +503,7 @@ def main():
             "clocks": clocks, "gpu_launches": KERNELS_PER_STEP * args.steps, "roofline": roofline,
             "host_polygen": {"seconds": prep_s, "workers": workers, "super_domains": batch.n_super,
                              "args_per_s": count / prep_s},
-            "e2e": e2e}
+            "e2e": e2e, "e2e_full": full}
     if not args.no_cpu_baseline and world == 1:  # rank 0 at N=1 only
         cb = cpu_baseline(args, batch, args.cpu_seconds)
         cb["counts_match_gpu"] = cb.pop("counts") == [int(counts[0]), int(counts[1]), int(counts[2])]

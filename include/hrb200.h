@@ -186,8 +186,10 @@ int hrb_run_slice(const hrb_slice* s, int algo, int mode, int split, const hrb_r
 /*
  * End-to-end variant with HOST buffers (pageable or pinned): copies the
  * slice to the device, runs hrb_run_slice, copies counts and candidates
- * back, synchronises.  Host outputs: counts[4], fail_ids (<= fail_cap),
- * cand_* (<= cand_cap).  Device buffers are cached per device and grown on
+ * back, synchronises.  Host outputs: counts[6] (hrb_run_slice's four, then
+ * the arguments covered by phase 2 and by phase 3 -- PhaseRow
+ * .arguments_covered, pipeline.py:440-451), fail_ids (<= fail_cap; NULL or
+ * fail_cap 0 skips that copy), cand_* (<= cand_cap).  Device buffers are cached per device and grown on
  * demand (a too-small internal subdomain buffer triggers one re-run).
  * For the regular family the upload is streamed behind the search (phase 1
  * waits per run of super-domains on a device counter) and the failing ids

@@ -93,7 +93,7 @@ def search_batch(algo: str, mode: int, one: int, a, b, eps, count):
 def _slice_args(batch):
     arrs = [np.ascontiguousarray(x) for x in (batch.coef, batch.G, batch.s2abs, batch.n_dom, batch.dom_n,
                                               batch.last_n)]
-    nu = np.ascontiguousarray(np.array([s.nu for s in batch.supers], dtype=np.uint32))
+    nu = np.ascontiguousarray(batch.nus, dtype=np.uint32)
     dom_id0 = np.ascontiguousarray((batch.dom_base[:-1] + np.uint64(batch.id0)).astype(np.uint64))
     m0 = np.ascontiguousarray(batch.m0)
     keep = arrs + [nu, dom_id0, m0]

@@ -22,6 +22,11 @@ LIB = os.path.join(LIBDIR, "libhrb200.so")
 PEAK_LIB = os.path.join(LIBDIR, "libhrbpeak.so")  # INT-pipe microbenchmark (roofline denominator)
 SOURCES = [os.path.join(CSRC, "hrb200.cu")]
 PEAK_SOURCES = [os.path.join(CSRC, "intpeak.cu")]
+HOST_LIB = os.path.join(LIBDIR, "libhrbhost.so")  # native host polygen + confirmation (no CUDA)
+HOST_SOURCES = [os.path.join(CSRC, "host", "hrb_host.cpp")]
+HOST_HEADERS = [os.path.join(CSRC, "host", f) for f in ("bign.h", "mpexp.h")] + [
+    os.path.join(ROOT, "include", "hrb_host.h")]
+HOST_FLAGS = ["-O3", "-std=c++17", "-fopenmp", "-fPIC", "-shared", "-Wall", "-Wextra", "-Wno-unused-parameter"]
 HEADERS = [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC)) if f.endswith((".cuh", ".h"))] + [
     os.path.join(ROOT, "include", "hrb200.h")]
 
@@ -75,13 +80,60 @@ def _compile(lib: str, sources: list, verbose: bool) -> None:
     os.replace(lib + ".srchash.tmp", lib + ".srchash")
 
 
+def cxx() -> str:
+    """The first C++ compiler that links -fopenmp (some images put a g++
+    without libgomp first in $CXX / on PATH)."""
+    for cand in (os.environ.get("CXX"), "/usr/bin/g++", shutil.which("g++")):
+        if not cand or not os.path.exists(cand):
+            continue
+        probe = subprocess.run([cand, "-fopenmp", "-x", "c++", "-", "-o", os.devnull], input="int main(){return 0;}",
+                               capture_output=True, text=True)
+        if probe.returncode == 0:
+            return cand
+    raise RuntimeError("no g++ with OpenMP found: needed for the native host library libhrbhost.so")
+
+
+def _host_hash() -> str:
+    import hashlib
+
+    h = hashlib.sha256(" ".join(HOST_FLAGS).encode())
+    for p in sorted(HOST_SOURCES + HOST_HEADERS):
+        with open(p, "rb") as fh:
+            h.update(os.path.basename(p).encode() + b"\0" + fh.read())
+    return h.hexdigest()[:32]
+
+
+def build_host(force: bool = False, verbose: bool = False) -> str:
+    """Compile libhrbhost.so (g++ -O3 -fopenmp) if missing or stale."""
+    stamp = HOST_LIB + ".srchash"
+    want = _host_hash()
+    if not force and os.path.exists(HOST_LIB) and os.path.exists(stamp) and open(stamp).read().strip() == want:
+        return HOST_LIB
+    os.makedirs(LIBDIR, exist_ok=True)
+    tmp = HOST_LIB + ".tmp"
+    cmd = [cxx(), *HOST_FLAGS, "-o", tmp, *HOST_SOURCES]
+    proc = subprocess.run(cmd, capture_output=True, text=True)
+    if proc.returncode != 0:
+        sys.stderr.write(proc.stdout + proc.stderr)
+        raise RuntimeError(f"g++ failed ({proc.returncode}): {' '.join(cmd)}")
+    if verbose:
+        sys.stderr.write(proc.stderr)
+    os.replace(tmp, HOST_LIB)
+    with open(stamp + ".tmp", "w") as fh:
+        fh.write(want)
+    os.replace(stamp + ".tmp", stamp)
+    return HOST_LIB
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     """Compile libhrb200.so (and the INT-peak probe libhrbpeak.so) for
-    sm_100a if missing or stale; return the main library's path."""
+    sm_100a, and the native host library, if missing or stale; return the
+    main library's path."""
     if force or _stale(LIB, SOURCES):
         _compile(LIB, SOURCES, verbose)
     if force or _stale(PEAK_LIB, PEAK_SOURCES):
         _compile(PEAK_LIB, PEAK_SOURCES, verbose)
+    build_host(force, verbose)
     return LIB
 
 

@@ -1582,8 +1582,45 @@ namespace {
 // phases 1-3 of a slice on `st`; ev_p1 (may be null) is recorded once the
 // phase-1 ids and count are final, so a caller can start copying them out
 // while phases 2 and 3 run.  Caller holds g_ws_mu.
+// Arguments covered by phases 2 and 3 (PhaseRow.arguments_covered,
+// pipeline.py:440-451): sum of the failing domains' sizes and of the
+// surviving subdomains' counts, so the host-buffer call returns the
+// reference's statistics without shipping the per-domain lists.
+__global__ void argsum_kernel(SliceDev s, int split, const uint64_t* fail_ids, const uint32_t* fail_t,
+                              const uint64_t* fail_count, uint64_t fail_cap, const uint64_t* sub_keys,
+                              const uint32_t* sub_t, const uint64_t* sub_count, uint64_t sub_cap,
+                              unsigned long long* out) {
+    uint64_t nf = *fail_count, ns = *sub_count;
+    if (nf > fail_cap) nf = fail_cap;
+    if (ns > sub_cap) ns = sub_cap;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    unsigned long long a2 = 0, a3 = 0;
+    for (uint64_t k = g; k < nf; k += stride) {
+        const int64_t t = fail_t[k];
+        a2 += domain_size(s, t, fail_ids[k] - s.dom_base[t]);
+    }
+    for (uint64_t k = g; k < ns; k += stride) {
+        const int64_t t = sub_t[k];
+        const uint64_t key = sub_keys[k];
+        const uint64_t n = domain_size(s, t, (key >> 8) - s.dom_base[t]);
+        uint64_t step = n / (uint64_t)split;
+        if (step < 1) step = 1;
+        const uint64_t start = (key & 255) * step;
+        a3 += step < n - start ? step : n - start;
+    }
+    for (int o = 16; o; o >>= 1) {
+        a2 += __shfl_down_sync(0xffffffffu, a2, o);
+        a3 += __shfl_down_sync(0xffffffffu, a3, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (a2) atomicAdd(&out[0], a2);
+        if (a3) atomicAdd(&out[1], a3);
+    }
+}
+
 int run_slice_locked(Workspace& ws, const hrb_slice* s, int algo, int mode, int split, const hrb_run_out* out,
-                     cudaStream_t st, cudaEvent_t ev_p1, const Stream& up = Stream()) {
+                     cudaStream_t st, cudaEvent_t ev_p1, const Stream& up = Stream(), uint64_t* argsums = nullptr) {
     int rc;
     SliceDev sd = to_dev(s);
     uint64_t* counts = out->counts;
@@ -1595,8 +1632,18 @@ int run_slice_locked(Workspace& ws, const hrb_slice* s, int algo, int mode, int 
     if ((rc = phase2_impl(ws, s, sd, algo, mode, split, out->fail_ids, (const uint32_t*)ws.fail_t.p, counts + 0,
                           out->fail_cap, out->sub_keys, counts + 1, out->sub_cap, st)))
         return rc;
-    return phase3_impl(ws, s, sd, split, out->sub_keys, (const uint32_t*)ws.sub_t.p, counts + 1, out->sub_cap,
-                       out->cand_index, out->cand_dist, out->cand_dom, counts + 2, out->cand_cap, st);
+    if ((rc = phase3_impl(ws, s, sd, split, out->sub_keys, (const uint32_t*)ws.sub_t.p, counts + 1, out->sub_cap,
+                          out->cand_index, out->cand_dist, out->cand_dom, counts + 2, out->cand_cap, st)))
+        return rc;
+    if (argsums) {
+        CK(cudaMemsetAsync(argsums, 0, sizeof(uint64_t) * 2, st));
+        argsum_kernel<<<sm_count() * 4, 256, 0, st>>>(sd, split, out->fail_ids, (const uint32_t*)ws.fail_t.p,
+                                                      counts + 0, out->fail_cap, out->sub_keys,
+                                                      (const uint32_t*)ws.sub_t.p, counts + 1, out->sub_cap,
+                                                      (unsigned long long*)argsums);
+        CK(cudaGetLastError());
+    }
+    return HRB_OK;
 }
 
 // hrb_run_slice replays its 17 launches as one CUDA graph when called again
@@ -1721,7 +1768,7 @@ int hrb_run_slice_host(const hrb_slice* hs, int algo, int mode, int split, uint6
     const size_t b_coef = sizeof(uint32_t) * 6 * CLd * S, b2 = sizeof(uint64_t) * 2 * S, b32 = sizeof(uint32_t) * S;
     if ((rc = H.coef.ensure(b_coef)) || (rc = H.G.ensure(b2)) || (rc = H.s2.ensure(b2)) || (rc = H.nd.ensure(b32)) ||
         (rc = H.dn.ensure(b32)) || (rc = H.ln.ensure(b32)) || (rc = H.db.ensure(sizeof(uint64_t) * (S + 1))) ||
-        (rc = H.m0.ensure(sizeof(uint64_t) * S)) || (rc = H.counts.ensure(sizeof(uint64_t) * 4)) ||
+        (rc = H.m0.ensure(sizeof(uint64_t) * S)) || (rc = H.counts.ensure(sizeof(uint64_t) * 6)) ||
         (rc = H.ready.ensure(2 * sizeof(uint32_t))))
         return rc;
     cudaStream_t st = H.st, cs = H.cs;
@@ -1816,7 +1863,7 @@ int hrb_run_slice_host(const hrb_slice* hs, int algo, int mode, int split, uint6
             if ((rc = check_slice(&ds)) || (rc = check_algo(algo, mode))) return rc;
             if (split < 2 || split > 64) return set_err(HRB_ERR_CONFIG, "phase2_split outside {2..64}");
             if ((rc = run_slice_locked(*ws, &ds, algo, mode, split, &o, st, fail_copied ? nullptr : H.ep1,
-                                       attempt == 0 ? up : Stream())))
+                                       attempt == 0 ? up : Stream(), (uint64_t*)H.counts.p + 4)))
                 return rc;
         }
         if (!fail_copied) {
@@ -1830,7 +1877,7 @@ int hrb_run_slice_host(const hrb_slice* hs, int algo, int mode, int split, uint6
                 CK(cudaMemcpyAsync(fail_ids, H.fail.p, sizeof(uint64_t) * nf0, cudaMemcpyDeviceToHost, H.cs));
             fail_copied = true;
         }
-        CK(cudaMemcpyAsync(counts, H.counts.p, sizeof(uint64_t) * 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(counts, H.counts.p, sizeof(uint64_t) * 6, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         if (counts[1] <= sub_cap) break;
         sub_cap = counts[1] + 1024;  // grow once and re-run

@@ -148,9 +148,13 @@ class FusedRunner:
                            _u64(self.cdom[:nc]), int(c[3]))
 
 
-def run_host(batch: SliceBatch, algo_code: int, mode_code: int, split: int, cand_cap: int = 1 << 16):
-    """hrb_run_slice_host: host buffers in, host results out (the e2e path).
-    Returns (counts, fail_ids, cand_index, cand_dist, cand_dom, device_ms)."""
+def run_host(batch: SliceBatch, algo_code: int, mode_code: int, split: int, cand_cap: int = 1 << 16,
+             with_fail_ids: bool = True):
+    """hrb_run_slice_host straight from the packed (pageable) host arrays:
+    streamed upload, phases 1-3, counts and candidates back (the e2e path).
+    Returns (counts[6], fail_ids, cand_index, cand_dist, cand_dom,
+    device_ms); with_fail_ids=False leaves the failing-domain list on the
+    device (fail_cap 0) and returns an empty array for it."""
     nat.require_cuda()
     lib = nat.load()
     arrs = [np.ascontiguousarray(a) for a in (batch.coef, batch.G, batch.s2abs, batch.n_dom, batch.dom_n,
@@ -160,22 +164,22 @@ def run_host(batch: SliceBatch, algo_code: int, mode_code: int, split: int, cand
                         coef_limbs=batch.coef_limbs, frac_bits=batch.frac_bits, word_bits=batch.word_bits,
                         delta=batch.delta, coef=p[0], G=p[1], s2abs=p[2], n_dom=p[3], dom_n=p[4], last_n=p[5],
                         dom_base=p[6], m0=p[7])
-    counts = np.zeros(4, dtype=np.uint64)
-    fail = np.zeros(max(batch.n_total, 1), dtype=np.uint64)
+    counts = np.zeros(6, dtype=np.uint64)
+    fail = np.zeros(max(batch.n_total, 1) if with_fail_ids else 1, dtype=np.uint64)
     while True:
-        cm = np.zeros(cand_cap, dtype=np.uint64)
-        cd = np.zeros(cand_cap, dtype=np.uint64)
-        cdom = np.zeros(cand_cap, dtype=np.uint64)
+        cm = np.zeros(max(cand_cap, 1), dtype=np.uint64)
+        cd = np.zeros(max(cand_cap, 1), dtype=np.uint64)
+        cdom = np.zeros(max(cand_cap, 1), dtype=np.uint64)
         ms = C.c_float(0)
-        rc = lib.hrb_run_slice_host(C.byref(desc), algo_code, mode_code, split, counts.ctypes.data, fail.ctypes.data,
-                                    fail.size, cm.ctypes.data, cd.ctypes.data, cdom.ctypes.data, cand_cap,
-                                    C.byref(ms))
+        rc = lib.hrb_run_slice_host(C.byref(desc), algo_code, mode_code, split, counts.ctypes.data,
+                                    fail.ctypes.data if with_fail_ids else None, fail.size if with_fail_ids else 0,
+                                    cm.ctypes.data, cd.ctypes.data, cdom.ctypes.data, cand_cap, C.byref(ms))
         if rc == nat.HRB_ERR_CAPACITY and counts[2] > cand_cap:
             cand_cap = int(counts[2])
             continue
         nat.check("hrb_run_slice_host", rc)
         break
-    nf, nc = int(counts[0]), int(counts[2])
+    nf, nc = (int(counts[0]) if with_fail_ids else 0), int(counts[2])
     return counts, fail[:nf], cm[:nc], cd[:nc], cdom[:nc], ms.value
 
 
@@ -210,7 +214,7 @@ class HostRunner:
                                  coef_limbs=batch.coef_limbs, frac_bits=batch.frac_bits, word_bits=batch.word_bits,
                                  delta=batch.delta, coef=p["coef"], G=p["G"], s2abs=p["s2abs"], n_dom=p["n_dom"],
                                  dom_n=p["dom_n"], last_n=p["last_n"], dom_base=p["dom_base"], m0=p["m0"])
-        self.counts = pinned((4,), np.uint64)
+        self.counts = pinned((6,), np.uint64)
         self.fail = pinned((max(batch.n_total, 1),), np.uint64)
         self._alloc_cands(cand_cap)
         self.device_ms = C.c_float(0)
@@ -248,7 +252,26 @@ class HostRunner:
 
     def output_bytes(self) -> int:
         """Bytes the last run() copied device -> host."""
-        return 32 + 8 * int(self.counts[0]) + 24 * min(int(self.counts[2]), self.cand_cap)
+        return 48 + 8 * int(self.counts[0]) + 24 * min(int(self.counts[2]), self.cand_cap)
+
+
+@dataclass
+class HostSliceResult:
+    """hrb_run_slice_host outputs without the per-domain lists."""
+
+    counts: np.ndarray        # uint64 [6]: fails, survivors, candidates, iterations, phase-2 args, phase-3 args
+    cand_index: np.ndarray
+    cand_dist: np.ndarray
+    cand_dom: np.ndarray
+    device_ms: float
+
+
+def run_slice_host(batch: SliceBatch, algo_code: int, mode_code: int, split: int,
+                   cand_cap: int = 1 << 16) -> HostSliceResult:
+    """run_host without the failing-domain list: what the end-to-end path
+    needs (counts, the arguments each phase covered, the candidates)."""
+    counts, _, cm, cd, cdom, ms = run_host(batch, algo_code, mode_code, split, cand_cap, with_fail_ids=False)
+    return HostSliceResult(counts, cm, cd, cdom, ms)
 
 
 def domain_coefficients(ds: DeviceSlice) -> np.ndarray:

@@ -136,15 +136,25 @@ def _resolve(cfg: PipelineConfig, algo: str | None) -> str:
 
 @dataclass
 class SliceOutput:
-    """Everything one slice produced, in the reference's types and order."""
+    """Everything one slice produced, in the reference's types and order.
+    The per-domain outputs stay numpy arrays (a 2^40 slice fails millions of
+    domains); failing_ids / sub_rows give the reference's list forms."""
 
     batch: SliceBatch
-    failing_ids: list          # phase-1 failing global domain ids (ascending)
-    sub_rows: list             # (parent id, sub index, start, count) ascending
+    fail_global: np.ndarray    # uint64 phase-1 failing global domain ids (ascending)
+    sub_table: tuple           # uint64 arrays (parent id, sub index, start, count), ascending
     candidates: list           # HrCaseRecord candidates of phase 3 (argument order)
     records: list              # confirmed HR records (sorted)
     stats: PhaseStats
     iterations: int            # phase-1 quotient steps (SearchOutcome.iterations)
+
+    @property
+    def failing_ids(self) -> list:
+        return self.fail_global.tolist()
+
+    @property
+    def sub_rows(self) -> list:
+        return list(zip(*(a.tolist() for a in self.sub_table)))
 
 
 def _sub_geometry(n: np.ndarray, j: np.ndarray, split: int):
@@ -155,7 +165,7 @@ def _sub_geometry(n: np.ndarray, j: np.ndarray, split: int):
 
 
 def execute_batch(batch: SliceBatch, cfg: PipelineConfig, algo: str, fn: str | None = None,
-                  confirm: bool = True) -> SliceOutput:
+                  confirm: bool = True, workers: int | None = None) -> SliceOutput:
     """Run phases 1-3 of a packed slice on the current CUDA device, then
     confirm the candidates on the host (pipeline.py:447-462)."""
     from .device import DeviceSlice, run_phases
@@ -186,11 +196,44 @@ def execute_batch(batch: SliceBatch, cfg: PipelineConfig, algo: str, fn: str | N
     records = []
     t4 = time.perf_counter()
     if confirm:
-        records = confirm_candidates(fn or cfg.fn, cand, fmt, cfg.phase.parallel_width)
+        records = confirm_candidates(fn or cfg.fn, cand, fmt, workers if workers is not None else
+                                     cfg.phase.parallel_width)
     stats.rows.append(PhaseRow("confirm", len(cand), len(records), len(cand), (time.perf_counter() - t4) * 1e3))
-    rows = list(zip((id0 + sub_local).tolist(), sub_j.tolist(), sub_start.tolist(), sub_cnt.tolist()))
-    return SliceOutput(batch, [id0 + int(x) for x in res.fail_ids.tolist()], rows, cand, records, stats,
-                       res.iterations)
+    table = (sub_local + np.uint64(id0), sub_j, sub_start, sub_cnt)
+    return SliceOutput(batch, res.fail_ids + np.uint64(id0), table, cand, records, stats, res.iterations)
+
+
+def execute_batch_host(batch: SliceBatch, cfg: PipelineConfig, algo: str, fn: str | None = None,
+                       confirm: bool = True, workers: int | None = None) -> SliceOutput:
+    """execute_batch through ONE host-buffer ABI call (hrb_run_slice_host:
+    streamed upload behind phase 1, all phases, counts and candidates back)
+    -- the path run_range takes.  The per-domain lists (failing ids,
+    subdomain rows) are not brought back: fail_global / sub_table are None;
+    the statistics (counts and arguments covered per phase) come from the
+    device.  The phase-1 row's wall_ms is the device time of all three
+    phases (the call does not split it)."""
+    from .device import run_slice_host
+
+    fmt = cfg.fmt
+    res = run_slice_host(batch, ALGO_CODE[Algorithm(algo)], MODE_CODE[cfg.phase.div_mode], cfg.phase.phase2_split)
+    n_fail, n_sub, n_cand, iters, a2, a3 = (int(x) for x in res.counts)
+    if batch.shift_bound_ok is not None and not batch.shift_bound_ok.all():
+        # the MPInt replay needs the failing ids: rare (narrow limb budgets)
+        return execute_batch(batch, cfg, algo, fn, confirm, workers)
+    id0 = batch.id0
+    stats = PhaseStats()
+    stats.rows.append(PhaseRow("phase1", batch.n_total, n_fail, batch.arguments, res.device_ms))
+    stats.rows.append(PhaseRow("phase2", n_fail, n_sub, a2, 0.0))
+    cand = [HrCaseRecord(index_bits(batch.binade, int(m), fmt), UFrac(int(dd), 64), id0 + int(dm))
+            for m, dd, dm in zip(res.cand_index.tolist(), res.cand_dist.tolist(), res.cand_dom.tolist())]
+    stats.rows.append(PhaseRow("phase3", n_sub, n_cand, a3, 0.0))
+    records = []
+    t4 = time.perf_counter()
+    if confirm:
+        records = confirm_candidates(fn or cfg.fn, cand, fmt, workers if workers is not None else
+                                     cfg.phase.parallel_width)
+    stats.rows.append(PhaseRow("confirm", len(cand), len(records), len(cand), (time.perf_counter() - t4) * 1e3))
+    return SliceOutput(batch, None, None, cand, records, stats, iters)
 
 
 def _confirm_chunk(job) -> list:
@@ -207,12 +250,47 @@ def _confirm_chunk(job) -> list:
 CONFIRM_CHUNK = 64
 
 
-def confirm_candidates(fn: str, cand: Sequence[HrCaseRecord], fmt: FpFormat, workers: int = 1) -> list:
+def _confirm_native(fn: str, cand: list, fmt: FpFormat, workers: int):
+    """hostgen.confirm on the candidates it covers; returns (records, rest)
+    where rest are the candidates for the exact Python path."""
+    from . import hostgen
+    from .fpformat import EXP_BIAS
+
+    p = fmt.precision
+    if fn not in hostgen.FN_CODES or not cand:
+        return [], cand
+    e = {c.argument >> (p - 1) for c in cand}
+    if len(e) != 1:
+        return [], cand
+    binade = e.pop() - EXP_BIAS - 1
+    if binade > 0:
+        return [], cand
+    pg = PolyGenConfig(delta=2)  # only precision / eps / binade matter to the confirmation
+    cfg = hostgen.make_cfg(fn, fmt, pg, binade, 64)
+    idx = np.array([c.argument & ((1 << (p - 1)) - 1) for c in cand], dtype=np.uint64)
+    is_hr, dist, status = hostgen.confirm(cfg, idx, workers)
+    records, rest = [], []
+    for c, h, d, st in zip(cand, is_hr.tolist(), dist.tolist(), status.tolist()):
+        if st != hostgen.HRBH_OK:
+            rest.append(c)
+        elif h:
+            records.append(HrCaseRecord(c.argument, UFrac(int(d), 64), c.domain_id))
+    return records, rest
+
+
+def confirm_candidates(fn: str, cand: Sequence[HrCaseRecord], fmt: FpFormat, workers: int = 1,
+                       native: bool | None = None) -> list:
     """Rigorous confirmation of phase-3 candidates (pipeline.py:447-462):
-    decide_hr at rising precision per candidate, records sorted.  The
-    candidates are independent, so workers > 1 spreads them over host
-    processes (the result is order-independent: it is sorted)."""
+    decide_hr at rising precision per candidate, records sorted.  exp on
+    binades <= 0 runs natively (hostgen, bit-identical decisions and
+    distances) over `workers` threads; everything else -- and any candidate
+    the native path hands back -- runs the Python decide_hr, spread over
+    host processes when workers > 1 (the result is sorted, so
+    order-independent)."""
     cand = list(cand)
+    native_recs = []
+    if native is not False:
+        native_recs, cand = _confirm_native(fn, cand, fmt, workers)
     if workers > 1 and len(cand) > 2 * CONFIRM_CHUNK:
         import multiprocessing as mp
 
@@ -221,24 +299,28 @@ def confirm_candidates(fn: str, cand: Sequence[HrCaseRecord], fmt: FpFormat, wor
             records = [r for part in pool.map(_confirm_chunk, jobs) for r in part]
     else:
         records = _confirm_chunk((fn, fmt, cand))
+    records.extend(native_recs)
     records.sort()
     return records
 
 
 def prepare_slice(fn: str, binade: int, start: int, count: int, cfg: PipelineConfig, workers: int | None = None,
-                  id0: int = 0) -> SliceBatch:
-    """Host half: Taylor blocks of the range, packed and checked."""
+                  id0: int = 0, native: bool | None = None) -> SliceBatch:
+    """Host half: Taylor blocks of the range, packed and checked (natively
+    where hostgen covers the configuration, else the exact Python path)."""
+    from .slices import pack_plan, plan_arrays
+
     w = workers if workers is not None else cfg.phase.parallel_width
-    supers = build_super_domains(fn, binade, cfg.fmt, cfg.polygen, start, count, workers=w, id0=id0)
     ceiling = cfg.phase.budgets.eps_dprime if cfg.phase.budgets is not None else None
-    return pack_slice(supers, cfg.fmt, cfg.polygen, cfg.word_bits, binade, budget_ceiling=ceiling, workers=w)
+    plan = plan_arrays(fn, binade, cfg.fmt, cfg.polygen, start, count, id0)
+    return pack_plan(plan, cfg.word_bits, budget_ceiling=ceiling, workers=w, native=native)
 
 
 def run_slice(fn: str, binade: int, start: int, count: int, cfg: PipelineConfig, algo: str | None = None,
               workers: int | None = None) -> SliceOutput:
     """The funnel over argument indices [start, start+count) of one binade."""
     batch = prepare_slice(fn, binade, start, count, cfg, workers)
-    return execute_batch(batch, cfg, _resolve(cfg, algo), fn)
+    return execute_batch(batch, cfg, _resolve(cfg, algo), fn, workers=workers)
 
 
 def run_pipeline(binade: int, cfg: PipelineConfig, prev_stats: PhaseStats | None = None):
@@ -346,7 +428,8 @@ def read_manifest(path: str, key: str) -> dict:
 
 
 def run_range(fn: str, binade: int, start: int, count: int, cfg: PipelineConfig, interval_args: int = 1 << 36,
-              workers: int | None = None, confirm: bool = True, manifest: str | None = None) -> RangeOutput:
+              workers: int | None = None, confirm: bool = True, manifest: str | None = None,
+              native: bool | None = None) -> RangeOutput:
     """A long argument range as consecutive intervals, the way the paper walks
     a binade: the block schedule of the WHOLE range is
     planned once (so blocks, domain ids and results are exactly those of a
@@ -360,18 +443,18 @@ def run_range(fn: str, binade: int, start: int, count: int, cfg: PipelineConfig,
     from concurrent.futures import ThreadPoolExecutor
 
     from .shard import partition_blocks
-    from .slices import pack_slice, plan_blocks, supers_of_blocks
+    from .slices import pack_plan, plan_arrays
 
     w = workers if workers is not None else cfg.phase.parallel_width
-    blocks = plan_blocks(fn, binade, cfg.fmt, cfg.polygen, start, count)
-    sizes = [b.bcount for b in blocks]
-    n_int = max(1, -(-sum(sizes) // max(1, interval_args)))
+    plan = plan_arrays(fn, binade, cfg.fmt, cfg.polygen, start, count)
+    sizes = plan.sizes
+    n_int = max(1, -(-int(sizes.sum()) // max(1, interval_args)))
     parts = [p for p in partition_blocks(sizes, n_int) if p[1] > p[0]]
     ceiling = cfg.phase.budgets.eps_dprime if cfg.phase.budgets is not None else None
+    bstart_of = [int(plan.bstart[p[0]]) for p in parts]
 
     def prepare(part):
-        supers = supers_of_blocks(blocks[part[0]:part[1]], w)
-        return pack_slice(supers, cfg.fmt, cfg.polygen, cfg.word_bits, binade, budget_ceiling=ceiling, workers=w)
+        return pack_plan(plan[part[0]:part[1]], cfg.word_bits, budget_ceiling=ceiling, workers=w, native=native)
 
     done, sink = {}, None
     if manifest is not None:
@@ -418,14 +501,14 @@ def run_range(fn: str, binade: int, start: int, count: int, cfg: PipelineConfig,
                 algo = cfg.phase.algorithm
                 if algo == "auto":
                     algo = select_algorithm(prev)
-                out = execute_batch(batch, cfg, algo, fn, confirm=confirm)
-                out.stats.algorithm_choices.append((blocks[part[0]].bstart, algo))
+                out = execute_batch_host(batch, cfg, algo, fn, confirm=confirm, workers=w)
+                out.stats.algorithm_choices.append((bstart_of[k], algo))
                 records.extend(out.records)
                 stats_list.append(out.stats)
-                choices.append((blocks[part[0]].bstart, algo))
+                choices.append((bstart_of[k], algo))
                 prev = out.stats
                 if sink is not None:
-                    sink.write(interval_line(k, blocks[part[0]].bstart, algo, out.records, out.stats) + "\n")
+                    sink.write(interval_line(k, bstart_of[k], algo, out.records, out.stats) + "\n")
                     sink.flush()
                     os.fsync(sink.fileno())
     finally:

@@ -143,7 +143,7 @@ def _run_rank(blocks, rank, world, fn, binade, cfg, algo, workers, confirm) -> S
     ceiling = cfg.phase.budgets.eps_dprime if cfg.phase.budgets is not None else None
     batch = pack_slice(supers, cfg.fmt, cfg.polygen, cfg.word_bits, binade, budget_ceiling=ceiling, workers=workers)
     out = execute_batch(batch, cfg, _resolve(cfg, algo), fn, confirm=confirm)
-    return ShardResult.of(len(out.failing_ids), len(out.sub_rows), out.candidates, out.records,
+    return ShardResult.of(len(out.fail_global), len(out.sub_table[0]), out.candidates, out.records,
                           out.iterations, batch.arguments)
 
 

@@ -274,6 +274,14 @@ class SliceBatch:
     m0: np.ndarray          # uint64 [S]
     id0: int = 0
     shift_bound_ok: np.ndarray = field(default=None)  # bool [S]
+    counts: np.ndarray = field(default=None)  # uint64 [S] arguments per super-domain
+    nus: np.ndarray = field(default=None)     # uint32 [S] packet length nu (the reference's packet walk)
+
+    def __post_init__(self) -> None:
+        if self.counts is None:
+            self.counts = np.array([s.count for s in self.supers], dtype=np.uint64)
+        if self.nus is None:
+            self.nus = np.array([s.nu for s in self.supers], dtype=np.uint32)
 
     @property
     def n_super(self) -> int:
@@ -293,7 +301,7 @@ class SliceBatch:
 
     @property
     def arguments(self) -> int:
-        return int(sum(s.count for s in self.supers))
+        return int(self.counts.sum())
 
     def locate(self, local_ids: np.ndarray):
         """(super index, domain index within it) of slice-local ids."""
@@ -399,8 +407,168 @@ def slice_view(batch: SliceBatch, t0: int, t1: int) -> SliceBatch:
                       np.ascontiguousarray(batch.G[:, t0:t1]), np.ascontiguousarray(batch.s2abs[:, t0:t1]),
                       batch.n_dom[t0:t1].copy(), batch.dom_n[t0:t1].copy(), batch.last_n[t0:t1].copy(),
                       db, batch.m0[t0:t1].copy(), id0=batch.id0 + int(batch.dom_base[t0]),
-                      shift_bound_ok=batch.shift_bound_ok[t0:t1].copy())
+                      shift_bound_ok=batch.shift_bound_ok[t0:t1].copy(), counts=batch.counts[t0:t1].copy(),
+                      nus=batch.nus[t0:t1].copy())
 
 
 def default_workers() -> int:
     return max(1, min(os.cpu_count() or 1, 64))
+
+
+# ------------------------------------------------- vectorised plan + native
+
+
+@dataclass
+class BlockPlan:
+    """The super-domain schedule of plan_blocks as columns (one entry per
+    block), so that a 2^40-argument range (65,536 blocks) is planned without
+    a Python object per block.  block(i) gives plan_blocks' _Block."""
+
+    fn: str
+    binade: int
+    fmt: FpFormat
+    pg: PolyGenConfig
+    bstart: np.ndarray    # uint64 binade index of the first argument
+    bcount: np.ndarray    # uint64 arguments
+    n_p: np.ndarray       # uint32 domain size
+    tau: np.ndarray       # uint32 domains
+    mu: np.ndarray        # uint32 packets
+    nu: np.ndarray        # uint32 domains per packet
+    e_out: np.ndarray     # int32 output exponent
+    dom_id0: np.ndarray   # uint64 first domain id
+
+    def __len__(self) -> int:
+        return len(self.bstart)
+
+    def __getitem__(self, sl: slice) -> "BlockPlan":
+        if not isinstance(sl, slice):
+            raise TypeError("BlockPlan slices only; use block(i)")
+        return BlockPlan(self.fn, self.binade, self.fmt, self.pg, *(getattr(self, k)[sl] for k in _PLAN_COLS))
+
+    @property
+    def sizes(self) -> np.ndarray:
+        return self.bcount
+
+    def block(self, i: int) -> _Block:
+        pg = self.pg
+        n_p, tau = int(self.n_p[i]), int(self.tau[i])
+        if int(self.bcount[i]) == pg.tau * n_p and n_p == pg.N:
+            bcfg = pg
+        else:
+            bcfg = PolyGenConfig(tau=tau, N=n_p, mu=1, nu=tau, delta=pg.delta, limbs=pg.limbs,
+                                 frac_bits=pg.frac_bits, guard=pg.guard)
+        return _Block(self.fn, self.binade, self.fmt, bcfg, int(self.bstart[i]), int(self.bcount[i]), n_p,
+                      int(self.e_out[i]), int(self.dom_id0[i]))
+
+
+_PLAN_COLS = ("bstart", "bcount", "n_p", "tau", "mu", "nu", "e_out", "dom_id0")
+
+
+def plan_arrays(fn: str, binade: int, fmt: FpFormat, pg: PolyGenConfig, start: int, count: int,
+                id0: int = 0) -> BlockPlan:
+    """plan_blocks as columns: the same blocks, sizes and domain ids."""
+    cols = {k: [] for k in _PLAN_COLS}
+    next_id = id0
+    for p_start, p_count, e_out in output_binade_pieces(fn, binade, fmt):
+        lo, hi = max(p_start, start), min(p_start + p_count, start + count)
+        if lo >= hi:
+            continue
+        piece = Domain((1 << (fmt.precision - 1)) + lo, binade + 1, hi - lo, 0)
+        n_p = piece_domain_size(fn, piece, e_out, fmt, pg.N)
+        block = pg.tau * n_p
+        bst = lo + np.arange(0, -(-(hi - lo) // block), dtype=np.uint64) * np.uint64(block)
+        bcnt = np.minimum(np.uint64(block), np.uint64(hi) - bst)
+        full = (bcnt == np.uint64(block)) & (n_p == pg.N)
+        tau_t = (bcnt + np.uint64(n_p - 1)) // np.uint64(n_p)
+        tau = np.where(full, np.uint64(pg.tau), tau_t).astype(np.uint32)
+        cols["bstart"].append(bst)
+        cols["bcount"].append(bcnt)
+        cols["n_p"].append(np.full(len(bst), n_p, dtype=np.uint32))
+        cols["tau"].append(tau)
+        cols["mu"].append(np.where(full, pg.mu, 1).astype(np.uint32))
+        cols["nu"].append(np.where(full, pg.nu, tau).astype(np.uint32))
+        cols["e_out"].append(np.full(len(bst), e_out, dtype=np.int32))
+        ids = np.zeros(len(bst), dtype=np.uint64)
+        np.cumsum(tau[:-1].astype(np.uint64), out=ids[1:])
+        cols["dom_id0"].append(ids + np.uint64(next_id))
+        next_id += int(tau.astype(np.uint64).sum())
+    dt = {"bstart": np.uint64, "bcount": np.uint64, "n_p": np.uint32, "tau": np.uint32, "mu": np.uint32,
+          "nu": np.uint32, "e_out": np.int32, "dom_id0": np.uint64}
+    return BlockPlan(fn, binade, fmt, pg, *(np.concatenate(cols[k]).astype(dt[k]) if cols[k]
+                                            else np.zeros(0, dt[k]) for k in _PLAN_COLS))
+
+
+def _signed_limbs(col: np.ndarray) -> int:
+    """Integer value of a two's-complement column of 32-bit limbs."""
+    v = 0
+    for k, w in enumerate(col.tolist()):
+        v |= int(w) << (32 * k)
+    bits = 32 * len(col)
+    return v - (1 << bits) if v >> (bits - 1) else v
+
+
+class PackedSupers:
+    """Sequence view of a natively packed slice's super-domains: SuperDomain
+    objects built on demand from the plan and the packed limbs (r_polys are
+    exact: L+1 two's-complement limbs hold every MPInt-valid coefficient).
+    eps_prime is not kept (the device reads G = ceil(eps' 2^F))."""
+
+    def __init__(self, plan: BlockPlan, coef: np.ndarray, delta: int):
+        self.plan, self.coef, self.delta = plan, coef, delta
+
+    def __len__(self) -> int:
+        return len(self.plan)
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return PackedSupers(self.plan[i], self.coef[:, :, i], self.delta)
+        if i < 0:
+            i += len(self)
+        pl = self.plan
+        vals = [_signed_limbs(self.coef[row, :, i]) for row in range(6)]
+        rows = [[vals[0], vals[1], vals[2]], [vals[3], vals[4]], [vals[5]]]
+        rp = tuple(BinomialPoly(tuple(rows[j][:self.delta - j + 1]), pl.pg.frac_bits) for j in range(self.delta + 1))
+        return SuperDomain(int(pl.bstart[i]), int(pl.bcount[i]), int(pl.n_p[i]), int(pl.tau[i]), int(pl.mu[i]),
+                           int(pl.nu[i]), int(pl.e_out[i]), int(pl.dom_id0[i]), rp, None)
+
+    def __iter__(self):
+        return (self[i] for i in range(len(self)))
+
+
+def pack_plan(plan: BlockPlan, word_bits: int, budget_ceiling: Fraction | None = None,
+              workers: int = 1, native: bool | None = None) -> SliceBatch:
+    """Taylor models + split + checks + packing of planned blocks.
+
+    With the native host library (hostgen: exp on binades <= 0, delta <= 2,
+    no budget ceiling) every block runs in C++ over `workers` host threads,
+    bit-identical to the Python path; blocks it flags go through the exact
+    Python path one by one (raising the reference's error where the
+    reference raises).  native=False forces the Python path."""
+    from . import hostgen
+
+    fmt, pg = plan.fmt, plan.pg
+    F = pg.frac_bits
+    if not len(plan):
+        raise ValueError("empty slice")
+    if not word_bits <= F <= 128:
+        raise ValueError(f"the B200 path needs word_bits <= frac_bits <= 128 (got F={F}, W={word_bits})")
+    use_native = hostgen.covers(plan.fn, plan.binade, fmt, pg, budget_ceiling) if native is None else native
+    if not use_native:
+        blocks = [plan.block(i) for i in range(len(plan))]
+        return pack_slice(supers_of_blocks(blocks, workers), fmt, pg, word_bits, plan.binade,
+                          budget_ceiling=budget_ceiling, workers=workers)
+    cfg = hostgen.make_cfg(plan.fn, fmt, pg, plan.binade, word_bits)
+    coef, G, s2, status, ok2 = hostgen.pack_columns(cfg, plan.bstart, plan.bcount, plan.n_p, plan.tau, plan.e_out,
+                                                    workers)
+    for t in np.flatnonzero(status != hostgen.HRBH_OK).tolist():
+        sd = _make_super(plan.block(t))  # exact Python path; raises where the reference raises
+        c1, g1, s21, _, k1 = _pack_rows([sd], fmt, pg, word_bits, budget_ceiling, True)
+        coef[:, :, t], G[:, t], s2[:, t], ok2[t] = c1[:, :, 0], g1[:, 0], s21[:, 0], k1[0]
+    n_dom = plan.tau.copy()
+    dom_n = plan.n_p.copy()
+    last_n = (plan.bcount - (plan.tau.astype(np.uint64) - np.uint64(1)) * plan.n_p.astype(np.uint64)).astype(np.uint32)
+    dom_base = np.zeros(len(plan) + 1, dtype=np.uint64)
+    np.cumsum(n_dom, out=dom_base[1:])
+    return SliceBatch(PackedSupers(plan, coef, pg.delta), fmt, plan.binade, F, word_bits, pg.delta, pg.limbs, coef,
+                      G, s2, n_dom, dom_n, last_n, dom_base, plan.bstart.copy(), id0=int(plan.dom_id0[0]),
+                      shift_bound_ok=ok2.astype(bool), counts=plan.bcount.copy(), nus=plan.nu.copy())

@@ -123,3 +123,10 @@ def test_run_range_threads_equal_run_slice():
     whole = run_slice("exp", 0, 0, 1 << 12, cfg, workers=1)
     ranged = run_range("exp", 0, 0, 1 << 12, cfg, interval_args=1 << 9, workers=1)
     assert ranged.records == whole.records
+    # the host-buffer call's device-side statistics equal the per-phase path's
+    for phase in ("phase1", "phase2", "phase3", "confirm"):
+        want = whole.stats.row(phase)
+        got = [st.row(phase) for st in ranged.interval_stats]
+        assert sum(r.domains_in for r in got) == want.domains_in, phase
+        assert sum(r.domains_out for r in got) == want.domains_out, phase
+        assert sum(r.arguments_covered for r in got) == want.arguments_covered, phase
