@@ -204,6 +204,61 @@ int hrb_run_slice_host(const hrb_slice* host_slice, int algo, int mode, int spli
                        uint64_t* cand_index, uint64_t* cand_dist, uint64_t* cand_dom,
                        uint64_t cand_cap, float* device_ms);
 
+/*
+ * High-degree slices (delta_R = degree in 3..8): one Taylor polynomial per
+ * large super-domain (up to 2^25 domains), the paper's large super-domain
+ * generation.  The reference rejects delta >= 3
+ * (polygen.py:81-82): this is an extension, specified by oracle/wide.py
+ * and produced by hrbh_wide_blocks (include/hrb_host.h).  F = 32 frac_limbs
+ * with frac_limbs = max(4, degree); residues are frac_limbs 32-bit limbs.
+ *
+ *   coef  uint32[(D+1)(D+2)/2][NL][S]  q_{j,l} = rho_{j,l} 2^F mod 2^F,
+ *         r_j(i) = sum_l q_{j,l} C(i, l) (binomial basis in the domain
+ *         index i), columns j-major (r_0's D+1, then r_1's D, ...)
+ *   padg  uint64[2][S]  ceil((ceil(eps' 2^F) + T3) / 2^(F-128)): eps' and
+ *         the degree >= 3 truncation bound, in 2^-128 units
+ *   s2b   uint64[2][S]  ceil(S2 / 2^(F-128)), S2 >= max_i |r_2(i)| 2^F
+ *   win   uint32[NL][S] ceil(eps' 2^F) + 1, the phase-3 window
+ *   geometry as hrb_slice
+ * Phases 1-2 test with pad = ceil((padg + s2b (n-1)^2) / 2^64) + n + 1.
+ */
+typedef struct hrb_wslice {
+    int64_t n_super;
+    int64_t n_total;
+    uint32_t max_dom_n; /* <= 2^16 */
+    int32_t degree;
+    int32_t frac_limbs;
+    int32_t word_bits; /* 64 */
+    const uint32_t* coef;
+    const uint64_t* padg;
+    const uint64_t* s2b;
+    const uint32_t* win;
+    const uint32_t* n_dom;
+    const uint32_t* dom_n;
+    const uint32_t* last_n;
+    const uint64_t* dom_base;
+    const uint64_t* m0;
+} hrb_wslice;
+
+/*
+ * Phases 1-3 of a high-degree slice on the device (hrb_run_slice's outputs
+ * and ordering): the tile columns of the multi-limb difference tables, the
+ * fused packet walk + Boolean test + regular search, phase 2 with the
+ * Toeplitz shift to the subdomain starts (split 2..16), the exact
+ * degree-delta_R phase-3 walk.  algo: HRB_ALGO_REGULAR or _UNROLLED.
+ */
+int hrb_wrun_slice(const hrb_wslice* s, int algo, int split, const hrb_run_out* out, void* stream);
+
+/* The same with HOST buffers in and out: counts[6] as hrb_run_slice_host. */
+int hrb_wrun_slice_host(const hrb_wslice* host_slice, int algo, int split, uint64_t* counts, uint64_t* cand_index,
+                        uint64_t* cand_dist, uint64_t* cand_dom, uint64_t cand_cap, float* device_ms);
+
+/*
+ * Tabulated values of a high-degree slice: every domain's (s_0..s_D) mod 2^F
+ * through the multi-limb packet walk.  out: uint32[D+1][NL][n_total].
+ */
+int hrb_wdomain_coefficients(const hrb_wslice* s, uint32_t* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

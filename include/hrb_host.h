@@ -71,6 +71,26 @@ int hrbh_confirm(const hrbh_cfg* cfg, int64_t n, const uint64_t* index, uint8_t*
                  uint8_t* status, int threads);
 
 /*
+ * High-degree super-domains (delta_R = degree in 3..8, F = 32 frac_limbs;
+ * the paper's large super-domain generation; the
+ * reference rejects delta >= 3, polygen.py:81-82, so this is an extension
+ * specified by oracle/wide.py).  Per block: the degree-delta_R Taylor
+ * model, its hierarchical split r_j(i) = Delta^j P(i N) in the binomial
+ * basis of the domain index, rounded once to 2^-F (the only rounding), the
+ * rigorous eps' (Lagrange + enclosure + rounding terms), and the device
+ * constants of include/hrb200.h hrb_wslice:
+ *   coef  uint32[(D+1)(D+2)/2][NL][S]  q_{j,l} mod 2^F, j-major
+ *   padg  uint64[2][S]  ceil((ceil(eps' 2^F) + T3) / 2^(F-128))
+ *   s2b   uint64[2][S]  ceil(S2 / 2^(F-128))
+ *   win   uint32[NL][S] ceil(eps' 2^F) + 1  (phase-3 window)
+ * exp on binades <= 0, W = 64.  status[t] = HRBH_FALLBACK when the block is
+ * out of range (budget eps'' >= 1/4, pad too wide, not covered).
+ */
+int hrbh_wide_blocks(const hrbh_cfg* cfg, int degree, int frac_limbs, int64_t S, const uint64_t* index_start,
+                     const uint64_t* count, const uint32_t* n_p, const uint32_t* tau, const int32_t* e_out,
+                     uint32_t* coef, uint64_t* padg, uint64_t* s2b, uint32_t* win, uint8_t* status, int threads);
+
+/*
  * The enclosure itself (for tests): exp(M 2^xe) at `prec` as
  * lo = lo_words * 2^lo_exp, hi = hi_words * 2^hi_exp (words little endian,
  * *nwords each, at most 16).  Returns HRBH_FALLBACK when not covered.

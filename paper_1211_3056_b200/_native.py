@@ -34,6 +34,9 @@ EXPORTS = (
     "hrb_phase3",
     "hrb_run_slice",
     "hrb_run_slice_host",
+    "hrb_wrun_slice",
+    "hrb_wrun_slice_host",
+    "hrb_wdomain_coefficients",
 )
 
 
@@ -49,6 +52,26 @@ class HrbSlice(C.Structure):
         ("coef", C.c_void_p),
         ("G", C.c_void_p),
         ("s2abs", C.c_void_p),
+        ("n_dom", C.c_void_p),
+        ("dom_n", C.c_void_p),
+        ("last_n", C.c_void_p),
+        ("dom_base", C.c_void_p),
+        ("m0", C.c_void_p),
+    ]
+
+
+class HrbWSlice(C.Structure):
+    _fields_ = [
+        ("n_super", C.c_int64),
+        ("n_total", C.c_int64),
+        ("max_dom_n", C.c_uint32),
+        ("degree", C.c_int32),
+        ("frac_limbs", C.c_int32),
+        ("word_bits", C.c_int32),
+        ("coef", C.c_void_p),
+        ("padg", C.c_void_p),
+        ("s2b", C.c_void_p),
+        ("win", C.c_void_p),
         ("n_dom", C.c_void_p),
         ("dom_n", C.c_void_p),
         ("last_n", C.c_void_p),
@@ -98,6 +121,9 @@ def _declare(lib) -> None:
     lib.hrb_run_slice.argtypes = [C.POINTER(HrbSlice), I, I, I, C.POINTER(HrbRunOut), P]
     lib.hrb_run_slice_host.argtypes = [C.POINTER(HrbSlice), I, I, I, P, P, U64, P, P, P, U64,
                                        C.POINTER(C.c_float)]
+    lib.hrb_wrun_slice.argtypes = [C.POINTER(HrbWSlice), I, I, C.POINTER(HrbRunOut), P]
+    lib.hrb_wrun_slice_host.argtypes = [C.POINTER(HrbWSlice), I, I, P, P, P, P, U64, C.POINTER(C.c_float)]
+    lib.hrb_wdomain_coefficients.argtypes = [C.POINTER(HrbWSlice), P, P]
     for name in EXPORTS:
         if name not in ("hrb_version", "hrb_last_error"):
             getattr(lib, name).restype = I

@@ -26,7 +26,8 @@ HOST_LIB = os.path.join(LIBDIR, "libhrbhost.so")  # native host polygen + confir
 HOST_SOURCES = [os.path.join(CSRC, "host", "hrb_host.cpp")]
 HOST_HEADERS = [os.path.join(CSRC, "host", f) for f in ("bign.h", "mpexp.h")] + [
     os.path.join(ROOT, "include", "hrb_host.h")]
-HOST_FLAGS = ["-O3", "-std=c++17", "-fopenmp", "-fPIC", "-shared", "-Wall", "-Wextra", "-Wno-unused-parameter"]
+HOST_FLAGS = ["-O3", "-std=c++17", "-fopenmp", "-fPIC", "-shared", "-Wall", "-Wextra", "-Wno-unused-parameter",
+              "-Wno-maybe-uninitialized"]
 HEADERS = [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC)) if f.endswith((".cuh", ".h"))] + [
     os.path.join(ROOT, "include", "hrb200.h")]
 

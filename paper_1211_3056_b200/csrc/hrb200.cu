@@ -1697,6 +1697,8 @@ int capture_run(GraphCache& G, Workspace& ws, const hrb_slice* s, int algo, int 
     G.valid = true;
     return HRB_OK;
 }
+
+#include "wide.cuh"
 }  // namespace
 
 extern "C" {
@@ -1897,6 +1899,136 @@ int hrb_run_slice_host(const hrb_slice* hs, int algo, int mode, int split, uint6
     if (device_ms) CK(cudaEventElapsedTime(device_ms, H.e0, H.e1));
     if (stream_in && *H.hflag) return set_err(HRB_ERR_RUNTIME, "streamed upload never arrived (wait_super timed out)");
     if (counts[0] > fail_cap && fail_ids) return set_err(HRB_ERR_CAPACITY, "fail_ids buffer too small");
+    if (counts[2] > cand_cap) return set_err(HRB_ERR_CAPACITY, "candidate buffer too small");
+    return HRB_OK;
+}
+
+}  // extern "C"
+
+// ===========================================================================
+// high-degree (delta_R >= 3) slices: include/hrb200.h hrb_wslice, csrc/wide.cuh
+// ===========================================================================
+extern "C" {
+
+int hrb_wrun_slice(const hrb_wslice* s, int algo, int split, const hrb_run_out* out, void* stream) {
+    int rc = check_wslice(s);
+    if (rc) return rc;
+    if (algo != hrb::ALGO_REGULAR && algo != hrb::ALGO_REGULAR_UNROLLED)
+        return set_err(HRB_ERR_CONFIG, "wide slices run the regular search family");
+    if (split < 2 || split > 16) return set_err(HRB_ERR_CONFIG, "wide slices need phase2_split in {2..16}");
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    Workspace* ws;
+    if ((rc = current_ws(&ws))) return rc;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    return run_wslice_locked(*ws, g_wws[dev & 63], s, algo, split, out, (cudaStream_t)stream, nullptr);
+}
+
+int hrb_wdomain_coefficients(const hrb_wslice* s, uint32_t* out, void* stream) {
+    int rc = check_wslice(s);
+    if (rc) return rc;
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    Workspace* ws;
+    if ((rc = current_ws(&ws))) return rc;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    return wtabdiff_impl(*ws, g_wws[dev & 63], s, out, (cudaStream_t)stream);
+}
+
+int hrb_wrun_slice_host(const hrb_wslice* hs, int algo, int split, uint64_t* counts, uint64_t* cand_index,
+                        uint64_t* cand_dist, uint64_t* cand_dom, uint64_t cand_cap, float* device_ms) {
+    int rc = check_wslice(hs);
+    if (rc) return rc;
+    if (algo != hrb::ALGO_REGULAR && algo != hrb::ALGO_REGULAR_UNROLLED)
+        return set_err(HRB_ERR_CONFIG, "wide slices run the regular search family");
+    if (split < 2 || split > 16) return set_err(HRB_ERR_CONFIG, "wide slices need phase2_split in {2..16}");
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> hl(g_host_mu[dev & 63]);
+    HostRunState& H = g_host[dev & 63];
+    if (!H.st) {
+        CK(cudaStreamCreateWithFlags(&H.st, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&H.cs, cudaStreamNonBlocking));
+        CK(cudaEventCreate(&H.e0));
+        CK(cudaEventCreate(&H.e1));
+        CK(cudaEventCreateWithFlags(&H.ep1, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&H.emeta, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&H.edata, cudaEventDisableTiming));
+        CK(cudaMallocHost((void**)&H.hcount, sizeof(uint64_t)));
+        CK(cudaMallocHost((void**)&H.hseq, sizeof(uint32_t) * UPLOAD_CHUNKS));
+        CK(cudaMallocHost((void**)&H.hflag, sizeof(uint32_t)));
+        for (int c = 0; c < UPLOAD_CHUNKS; c++) H.hseq[c] = (uint32_t)(c + 1);
+    }
+    const int64_t S = hs->n_super, NT = hs->n_total;
+    const int D = hs->degree, NL = hs->frac_limbs, ncoef = (D + 1) * (D + 2) / 2;
+    const size_t b_coef = sizeof(uint32_t) * ncoef * NL * S, b2 = sizeof(uint64_t) * 2 * S,
+                 b32 = sizeof(uint32_t) * S, b_win = sizeof(uint32_t) * NL * S;
+    // the host-state buffers are reused: coef, G <- padg, s2 <- s2b, ready <- win
+    if ((rc = H.coef.ensure(b_coef)) || (rc = H.G.ensure(b2)) || (rc = H.s2.ensure(b2)) || (rc = H.ready.ensure(b_win)) ||
+        (rc = H.nd.ensure(b32)) || (rc = H.dn.ensure(b32)) || (rc = H.ln.ensure(b32)) ||
+        (rc = H.db.ensure(sizeof(uint64_t) * (S + 1))) || (rc = H.m0.ensure(sizeof(uint64_t) * S)) ||
+        (rc = H.counts.ensure(sizeof(uint64_t) * 6)))
+        return rc;
+    cudaStream_t st = H.st;
+    CK(cudaEventRecord(H.e0, st));
+    CK(cudaMemcpyAsync(H.coef.p, hs->coef, b_coef, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(H.G.p, hs->padg, b2, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(H.s2.p, hs->s2b, b2, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(H.ready.p, hs->win, b_win, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(H.nd.p, hs->n_dom, b32, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(H.dn.p, hs->dom_n, b32, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(H.ln.p, hs->last_n, b32, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(H.db.p, hs->dom_base, sizeof(uint64_t) * (S + 1), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(H.m0.p, hs->m0, sizeof(uint64_t) * S, cudaMemcpyHostToDevice, st));
+    hrb_wslice ds = *hs;
+    ds.coef = (const uint32_t*)H.coef.p;
+    ds.padg = (const uint64_t*)H.G.p;
+    ds.s2b = (const uint64_t*)H.s2.p;
+    ds.win = (const uint32_t*)H.ready.p;
+    ds.n_dom = (const uint32_t*)H.nd.p;
+    ds.dom_n = (const uint32_t*)H.dn.p;
+    ds.last_n = (const uint32_t*)H.ln.p;
+    ds.dom_base = (const uint64_t*)H.db.p;
+    ds.m0 = (const uint64_t*)H.m0.p;
+    uint64_t sub_cap = (uint64_t)NT / 8 + 1024;
+    const uint64_t fcap = (uint64_t)NT;
+    for (int attempt = 0; attempt < 2; attempt++) {
+        if ((rc = H.fail.ensure(sizeof(uint64_t) * (fcap + 1))) || (rc = H.sub.ensure(sizeof(uint64_t) * (sub_cap + 1))) ||
+            (rc = H.cm.ensure(sizeof(uint64_t) * (cand_cap + 1))) ||
+            (rc = H.cd.ensure(sizeof(uint64_t) * (cand_cap + 1))) ||
+            (rc = H.cdom.ensure(sizeof(uint64_t) * (cand_cap + 1))))
+            return rc;
+        hrb_run_out o;
+        o.fail_ids = (uint64_t*)H.fail.p;
+        o.fail_cap = fcap;
+        o.sub_keys = (uint64_t*)H.sub.p;
+        o.sub_cap = sub_cap;
+        o.cand_index = (uint64_t*)H.cm.p;
+        o.cand_dist = (uint64_t*)H.cd.p;
+        o.cand_dom = (uint64_t*)H.cdom.p;
+        o.cand_cap = cand_cap;
+        o.counts = (uint64_t*)H.counts.p;
+        {
+            std::lock_guard<std::mutex> lk(g_ws_mu);
+            Workspace* ws;
+            if ((rc = current_ws(&ws))) return rc;
+            if ((rc = run_wslice_locked(*ws, g_wws[dev & 63], &ds, algo, split, &o, st, (uint64_t*)H.counts.p + 4)))
+                return rc;
+        }
+        CK(cudaMemcpyAsync(counts, H.counts.p, sizeof(uint64_t) * 6, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (counts[1] <= sub_cap) break;
+        sub_cap = counts[1] + 1024;
+    }
+    const uint64_t nc = counts[2] < cand_cap ? counts[2] : cand_cap;
+    if (nc) {
+        CK(cudaMemcpyAsync(cand_index, H.cm.p, sizeof(uint64_t) * nc, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(cand_dist, H.cd.p, sizeof(uint64_t) * nc, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(cand_dom, H.cdom.p, sizeof(uint64_t) * nc, cudaMemcpyDeviceToHost, st));
+    }
+    CK(cudaEventRecord(H.e1, st));
+    CK(cudaStreamSynchronize(st));
+    if (device_ms) CK(cudaEventElapsedTime(device_ms, H.e0, H.e1));
     if (counts[2] > cand_cap) return set_err(HRB_ERR_CAPACITY, "candidate buffer too small");
     return HRB_OK;
 }

@@ -49,6 +49,8 @@ def load():
             lib.hrbh_pack_blocks.restype = I
             lib.hrbh_confirm.argtypes = [C.POINTER(HrbhCfg), I64, P, P, P, P, I]
             lib.hrbh_confirm.restype = I
+            lib.hrbh_wide_blocks.argtypes = [C.POINTER(HrbhCfg), I, I, I64, P, P, P, P, P, P, P, P, P, P, I]
+            lib.hrbh_wide_blocks.restype = I
             lib.hrbh_exp_enclose.argtypes = [C.c_uint64, I, I, P, P, P, P, P]
             lib.hrbh_exp_enclose.restype = I
             _lib = lib
@@ -89,6 +91,28 @@ def pack_columns(cfg: HrbhCfg, index_start, count, n_p, tau, e_out, workers: int
     if rc:
         raise ValueError(f"hrbh_pack_blocks rejected the configuration (status {rc})")
     return coef, G, s2, status, ok2
+
+
+def wide_columns(cfg: HrbhCfg, degree: int, frac_limbs: int, index_start, count, n_p, tau, e_out,
+                 workers: int = 0):
+    """hrbh_wide_blocks over S blocks: (coef [(D+1)(D+2)/2, NL, S] u32,
+    padg [2, S], s2b [2, S], win [NL, S] u32, status [S])."""
+    lib = load()
+    S = len(index_start)
+    cols = [np.ascontiguousarray(index_start, dtype=np.uint64), np.ascontiguousarray(count, dtype=np.uint64),
+            np.ascontiguousarray(n_p, dtype=np.uint32), np.ascontiguousarray(tau, dtype=np.uint32),
+            np.ascontiguousarray(e_out, dtype=np.int32)]
+    ncoef = (degree + 1) * (degree + 2) // 2
+    coef = np.zeros((ncoef, frac_limbs, S), dtype=np.uint32)
+    padg = np.zeros((2, S), dtype=np.uint64)
+    s2b = np.zeros((2, S), dtype=np.uint64)
+    win = np.zeros((frac_limbs, S), dtype=np.uint32)
+    status = np.zeros(S, dtype=np.uint8)
+    rc = lib.hrbh_wide_blocks(C.byref(cfg), degree, frac_limbs, S, *(_ptr(a) for a in cols), _ptr(coef),
+                              _ptr(padg), _ptr(s2b), _ptr(win), _ptr(status), int(workers))
+    if rc:
+        raise ValueError(f"hrbh_wide_blocks rejected the configuration (status {rc})")
+    return coef, padg, s2b, win, status
 
 
 def confirm(cfg: HrbhCfg, index: np.ndarray, workers: int = 0):

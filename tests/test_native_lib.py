@@ -47,3 +47,33 @@ def test_config_errors_do_not_need_a_gpu():
     rc = lib.hrb_search_batch(9, 0, 64, 0, None, None, None, None, None, None, None, None, None, None)
     assert rc == _native.HRB_ERR_CONFIG
     assert b"algorithm" in lib.hrb_last_error()
+
+
+def host_declared_symbols() -> list[str]:
+    text = open(os.path.join(ROOT, "include", "hrb_host.h")).read()
+    return sorted(set(re.findall(r"^int\s+(hrbh_\w+)\s*\(", text, re.M)))
+
+
+def test_host_library_exports_all_symbols():
+    """libhrbhost.so (native host generation + confirmation) exports every
+    entry point of include/hrb_host.h and loads without a GPU."""
+    from paper_1211_3056_b200 import hostgen
+    from paper_1211_3056_b200.build import HOST_LIB, build_host
+
+    build_host()
+    out = subprocess.run(["nm", "-D", "--defined-only", HOST_LIB], capture_output=True, text=True,
+                         check=True).stdout
+    exported = set(re.findall(r" T (hrbh_\w+)", out))
+    want = set(host_declared_symbols())
+    assert want and not (want - exported), want - exported
+    assert hostgen.load().hrbh_version() == 100
+
+
+def test_wide_config_errors_do_not_need_a_gpu():
+    import ctypes as C
+
+    lib = _native.load()
+    bad = _native.HrbWSlice(n_super=1, n_total=1, max_dom_n=8, degree=2, frac_limbs=4, word_bits=64)
+    out = _native.HrbRunOut()
+    assert lib.hrb_wrun_slice(C.byref(bad), 2, 8, C.byref(out), None) == _native.HRB_ERR_CONFIG
+    assert b"degree" in lib.hrb_last_error()
