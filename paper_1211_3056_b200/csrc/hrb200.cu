@@ -975,13 +975,241 @@ __global__ void scatter3_kernel(const Cand* app, const unsigned long long* app_c
 // ---------------------------------------------------------------------------
 // full-width tabulated differences (domain_coefficient_sets parity)
 // ---------------------------------------------------------------------------
-// x += y over CL limbs with one add-with-carry chain (IADD3 / IADD3.X)
+// x += y over CL limbs with one add-with-carry chain (IADD3 / IADD3.X).
+// ONE asm statement per chain: the carry flag does not survive between
+// separate asm statements (the compiler may schedule another chain's
+// add.cc in between), so every width gets its own single-statement body.
 template <int CL>
-__device__ __forceinline__ void addc_chain(uint32_t (&x)[CL], const uint32_t (&y)[CL]) {
-    asm("add.cc.u32 %0, %0, %1;" : "+r"(x[0]) : "r"(y[0]));
-#pragma unroll
-    for (int l = 1; l < CL - 1; l++) asm("addc.cc.u32 %0, %0, %1;" : "+r"(x[l]) : "r"(y[l]));
-    if (CL > 1) asm("addc.u32 %0, %0, %1;" : "+r"(x[CL - 1]) : "r"(y[CL - 1]));
+__device__ __forceinline__ void addc_chain(uint32_t (&x)[CL], const uint32_t (&y)[CL]);
+
+template <>
+__device__ __forceinline__ void addc_chain<1>(uint32_t (&x)[1], const uint32_t (&y)[1]) {
+    x[0] += y[0];
+}
+
+template <>
+__device__ __forceinline__ void addc_chain<2>(uint32_t (&x)[2], const uint32_t (&y)[2]) {
+    asm("add.cc.u32 %0, %0, %2;\n\t"
+        "addc.u32 %1, %1, %3;"
+        : "+r"(x[0]), "+r"(x[1])
+        : "r"(y[0]), "r"(y[1]));
+}
+
+template <>
+__device__ __forceinline__ void addc_chain<3>(uint32_t (&x)[3], const uint32_t (&y)[3]) {
+    asm("add.cc.u32 %0, %0, %3;\n\t"
+        "addc.cc.u32 %1, %1, %4;\n\t"
+        "addc.u32 %2, %2, %5;"
+        : "+r"(x[0]), "+r"(x[1]), "+r"(x[2])
+        : "r"(y[0]), "r"(y[1]), "r"(y[2]));
+}
+
+template <>
+__device__ __forceinline__ void addc_chain<4>(uint32_t (&x)[4], const uint32_t (&y)[4]) {
+    asm("add.cc.u32 %0, %0, %4;\n\t"
+        "addc.cc.u32 %1, %1, %5;\n\t"
+        "addc.cc.u32 %2, %2, %6;\n\t"
+        "addc.u32 %3, %3, %7;"
+        : "+r"(x[0]), "+r"(x[1]), "+r"(x[2]), "+r"(x[3])
+        : "r"(y[0]), "r"(y[1]), "r"(y[2]), "r"(y[3]));
+}
+
+template <>
+__device__ __forceinline__ void addc_chain<5>(uint32_t (&x)[5], const uint32_t (&y)[5]) {
+    asm("add.cc.u32 %0, %0, %5;\n\t"
+        "addc.cc.u32 %1, %1, %6;\n\t"
+        "addc.cc.u32 %2, %2, %7;\n\t"
+        "addc.cc.u32 %3, %3, %8;\n\t"
+        "addc.u32 %4, %4, %9;"
+        : "+r"(x[0]), "+r"(x[1]), "+r"(x[2]), "+r"(x[3]), "+r"(x[4])
+        : "r"(y[0]), "r"(y[1]), "r"(y[2]), "r"(y[3]), "r"(y[4]));
+}
+
+template <>
+__device__ __forceinline__ void addc_chain<6>(uint32_t (&x)[6], const uint32_t (&y)[6]) {
+    asm("add.cc.u32 %0, %0, %6;\n\t"
+        "addc.cc.u32 %1, %1, %7;\n\t"
+        "addc.cc.u32 %2, %2, %8;\n\t"
+        "addc.cc.u32 %3, %3, %9;\n\t"
+        "addc.cc.u32 %4, %4, %10;\n\t"
+        "addc.u32 %5, %5, %11;"
+        : "+r"(x[0]), "+r"(x[1]), "+r"(x[2]), "+r"(x[3]), "+r"(x[4]), "+r"(x[5])
+        : "r"(y[0]), "r"(y[1]), "r"(y[2]), "r"(y[3]), "r"(y[4]), "r"(y[5]));
+}
+
+template <>
+__device__ __forceinline__ void addc_chain<7>(uint32_t (&x)[7], const uint32_t (&y)[7]) {
+    asm("add.cc.u32 %0, %0, %7;\n\t"
+        "addc.cc.u32 %1, %1, %8;\n\t"
+        "addc.cc.u32 %2, %2, %9;\n\t"
+        "addc.cc.u32 %3, %3, %10;\n\t"
+        "addc.cc.u32 %4, %4, %11;\n\t"
+        "addc.cc.u32 %5, %5, %12;\n\t"
+        "addc.u32 %6, %6, %13;"
+        : "+r"(x[0]), "+r"(x[1]), "+r"(x[2]), "+r"(x[3]), "+r"(x[4]), "+r"(x[5]), "+r"(x[6])
+        : "r"(y[0]), "r"(y[1]), "r"(y[2]), "r"(y[3]), "r"(y[4]), "r"(y[5]), "r"(y[6]));
+}
+
+template <>
+__device__ __forceinline__ void addc_chain<8>(uint32_t (&x)[8], const uint32_t (&y)[8]) {
+    asm("add.cc.u32 %0, %0, %8;\n\t"
+        "addc.cc.u32 %1, %1, %9;\n\t"
+        "addc.cc.u32 %2, %2, %10;\n\t"
+        "addc.cc.u32 %3, %3, %11;\n\t"
+        "addc.cc.u32 %4, %4, %12;\n\t"
+        "addc.cc.u32 %5, %5, %13;\n\t"
+        "addc.cc.u32 %6, %6, %14;\n\t"
+        "addc.u32 %7, %7, %15;"
+        : "+r"(x[0]), "+r"(x[1]), "+r"(x[2]), "+r"(x[3]), "+r"(x[4]), "+r"(x[5]), "+r"(x[6]), "+r"(x[7])
+        : "r"(y[0]), "r"(y[1]), "r"(y[2]), "r"(y[3]), "r"(y[4]), "r"(y[5]), "r"(y[6]), "r"(y[7]));
+}
+
+template <>
+__device__ __forceinline__ void addc_chain<9>(uint32_t (&x)[9], const uint32_t (&y)[9]) {
+    asm("add.cc.u32 %0, %0, %9;\n\t"
+        "addc.cc.u32 %1, %1, %10;\n\t"
+        "addc.cc.u32 %2, %2, %11;\n\t"
+        "addc.cc.u32 %3, %3, %12;\n\t"
+        "addc.cc.u32 %4, %4, %13;\n\t"
+        "addc.cc.u32 %5, %5, %14;\n\t"
+        "addc.cc.u32 %6, %6, %15;\n\t"
+        "addc.cc.u32 %7, %7, %16;\n\t"
+        "addc.u32 %8, %8, %17;"
+        : "+r"(x[0]), "+r"(x[1]), "+r"(x[2]), "+r"(x[3]), "+r"(x[4]), "+r"(x[5]), "+r"(x[6]), "+r"(x[7]), "+r"(x[8])
+        : "r"(y[0]), "r"(y[1]), "r"(y[2]), "r"(y[3]), "r"(y[4]), "r"(y[5]), "r"(y[6]), "r"(y[7]), "r"(y[8]));
+}
+
+template <>
+__device__ __forceinline__ void addc_chain<10>(uint32_t (&x)[10], const uint32_t (&y)[10]) {
+    asm("add.cc.u32 %0, %0, %10;\n\t"
+        "addc.cc.u32 %1, %1, %11;\n\t"
+        "addc.cc.u32 %2, %2, %12;\n\t"
+        "addc.cc.u32 %3, %3, %13;\n\t"
+        "addc.cc.u32 %4, %4, %14;\n\t"
+        "addc.cc.u32 %5, %5, %15;\n\t"
+        "addc.cc.u32 %6, %6, %16;\n\t"
+        "addc.cc.u32 %7, %7, %17;\n\t"
+        "addc.cc.u32 %8, %8, %18;\n\t"
+        "addc.u32 %9, %9, %19;"
+        : "+r"(x[0]), "+r"(x[1]), "+r"(x[2]), "+r"(x[3]), "+r"(x[4]), "+r"(x[5]), "+r"(x[6]), "+r"(x[7]), "+r"(x[8]), "+r"(x[9])
+        : "r"(y[0]), "r"(y[1]), "r"(y[2]), "r"(y[3]), "r"(y[4]), "r"(y[5]), "r"(y[6]), "r"(y[7]), "r"(y[8]), "r"(y[9]));
+}
+
+template <>
+__device__ __forceinline__ void addc_chain<11>(uint32_t (&x)[11], const uint32_t (&y)[11]) {
+    asm("add.cc.u32 %0, %0, %11;\n\t"
+        "addc.cc.u32 %1, %1, %12;\n\t"
+        "addc.cc.u32 %2, %2, %13;\n\t"
+        "addc.cc.u32 %3, %3, %14;\n\t"
+        "addc.cc.u32 %4, %4, %15;\n\t"
+        "addc.cc.u32 %5, %5, %16;\n\t"
+        "addc.cc.u32 %6, %6, %17;\n\t"
+        "addc.cc.u32 %7, %7, %18;\n\t"
+        "addc.cc.u32 %8, %8, %19;\n\t"
+        "addc.cc.u32 %9, %9, %20;\n\t"
+        "addc.u32 %10, %10, %21;"
+        : "+r"(x[0]), "+r"(x[1]), "+r"(x[2]), "+r"(x[3]), "+r"(x[4]), "+r"(x[5]), "+r"(x[6]), "+r"(x[7]), "+r"(x[8]), "+r"(x[9]), "+r"(x[10])
+        : "r"(y[0]), "r"(y[1]), "r"(y[2]), "r"(y[3]), "r"(y[4]), "r"(y[5]), "r"(y[6]), "r"(y[7]), "r"(y[8]), "r"(y[9]), "r"(y[10]));
+}
+
+template <>
+__device__ __forceinline__ void addc_chain<12>(uint32_t (&x)[12], const uint32_t (&y)[12]) {
+    asm("add.cc.u32 %0, %0, %12;\n\t"
+        "addc.cc.u32 %1, %1, %13;\n\t"
+        "addc.cc.u32 %2, %2, %14;\n\t"
+        "addc.cc.u32 %3, %3, %15;\n\t"
+        "addc.cc.u32 %4, %4, %16;\n\t"
+        "addc.cc.u32 %5, %5, %17;\n\t"
+        "addc.cc.u32 %6, %6, %18;\n\t"
+        "addc.cc.u32 %7, %7, %19;\n\t"
+        "addc.cc.u32 %8, %8, %20;\n\t"
+        "addc.cc.u32 %9, %9, %21;\n\t"
+        "addc.cc.u32 %10, %10, %22;\n\t"
+        "addc.u32 %11, %11, %23;"
+        : "+r"(x[0]), "+r"(x[1]), "+r"(x[2]), "+r"(x[3]), "+r"(x[4]), "+r"(x[5]), "+r"(x[6]), "+r"(x[7]), "+r"(x[8]), "+r"(x[9]), "+r"(x[10]), "+r"(x[11])
+        : "r"(y[0]), "r"(y[1]), "r"(y[2]), "r"(y[3]), "r"(y[4]), "r"(y[5]), "r"(y[6]), "r"(y[7]), "r"(y[8]), "r"(y[9]), "r"(y[10]), "r"(y[11]));
+}
+
+template <>
+__device__ __forceinline__ void addc_chain<13>(uint32_t (&x)[13], const uint32_t (&y)[13]) {
+    asm("add.cc.u32 %0, %0, %13;\n\t"
+        "addc.cc.u32 %1, %1, %14;\n\t"
+        "addc.cc.u32 %2, %2, %15;\n\t"
+        "addc.cc.u32 %3, %3, %16;\n\t"
+        "addc.cc.u32 %4, %4, %17;\n\t"
+        "addc.cc.u32 %5, %5, %18;\n\t"
+        "addc.cc.u32 %6, %6, %19;\n\t"
+        "addc.cc.u32 %7, %7, %20;\n\t"
+        "addc.cc.u32 %8, %8, %21;\n\t"
+        "addc.cc.u32 %9, %9, %22;\n\t"
+        "addc.cc.u32 %10, %10, %23;\n\t"
+        "addc.cc.u32 %11, %11, %24;\n\t"
+        "addc.u32 %12, %12, %25;"
+        : "+r"(x[0]), "+r"(x[1]), "+r"(x[2]), "+r"(x[3]), "+r"(x[4]), "+r"(x[5]), "+r"(x[6]), "+r"(x[7]), "+r"(x[8]), "+r"(x[9]), "+r"(x[10]), "+r"(x[11]), "+r"(x[12])
+        : "r"(y[0]), "r"(y[1]), "r"(y[2]), "r"(y[3]), "r"(y[4]), "r"(y[5]), "r"(y[6]), "r"(y[7]), "r"(y[8]), "r"(y[9]), "r"(y[10]), "r"(y[11]), "r"(y[12]));
+}
+
+template <>
+__device__ __forceinline__ void addc_chain<14>(uint32_t (&x)[14], const uint32_t (&y)[14]) {
+    asm("add.cc.u32 %0, %0, %14;\n\t"
+        "addc.cc.u32 %1, %1, %15;\n\t"
+        "addc.cc.u32 %2, %2, %16;\n\t"
+        "addc.cc.u32 %3, %3, %17;\n\t"
+        "addc.cc.u32 %4, %4, %18;\n\t"
+        "addc.cc.u32 %5, %5, %19;\n\t"
+        "addc.cc.u32 %6, %6, %20;\n\t"
+        "addc.cc.u32 %7, %7, %21;\n\t"
+        "addc.cc.u32 %8, %8, %22;\n\t"
+        "addc.cc.u32 %9, %9, %23;\n\t"
+        "addc.cc.u32 %10, %10, %24;\n\t"
+        "addc.cc.u32 %11, %11, %25;\n\t"
+        "addc.cc.u32 %12, %12, %26;\n\t"
+        "addc.u32 %13, %13, %27;"
+        : "+r"(x[0]), "+r"(x[1]), "+r"(x[2]), "+r"(x[3]), "+r"(x[4]), "+r"(x[5]), "+r"(x[6]), "+r"(x[7]), "+r"(x[8]), "+r"(x[9]), "+r"(x[10]), "+r"(x[11]), "+r"(x[12]), "+r"(x[13])
+        : "r"(y[0]), "r"(y[1]), "r"(y[2]), "r"(y[3]), "r"(y[4]), "r"(y[5]), "r"(y[6]), "r"(y[7]), "r"(y[8]), "r"(y[9]), "r"(y[10]), "r"(y[11]), "r"(y[12]), "r"(y[13]));
+}
+
+template <>
+__device__ __forceinline__ void addc_chain<15>(uint32_t (&x)[15], const uint32_t (&y)[15]) {
+    asm("add.cc.u32 %0, %0, %15;\n\t"
+        "addc.cc.u32 %1, %1, %16;\n\t"
+        "addc.cc.u32 %2, %2, %17;\n\t"
+        "addc.cc.u32 %3, %3, %18;\n\t"
+        "addc.cc.u32 %4, %4, %19;\n\t"
+        "addc.cc.u32 %5, %5, %20;\n\t"
+        "addc.cc.u32 %6, %6, %21;\n\t"
+        "addc.cc.u32 %7, %7, %22;\n\t"
+        "addc.cc.u32 %8, %8, %23;\n\t"
+        "addc.cc.u32 %9, %9, %24;\n\t"
+        "addc.cc.u32 %10, %10, %25;\n\t"
+        "addc.cc.u32 %11, %11, %26;\n\t"
+        "addc.cc.u32 %12, %12, %27;\n\t"
+        "addc.cc.u32 %13, %13, %28;\n\t"
+        "addc.u32 %14, %14, %29;"
+        : "+r"(x[0]), "+r"(x[1]), "+r"(x[2]), "+r"(x[3]), "+r"(x[4]), "+r"(x[5]), "+r"(x[6]), "+r"(x[7]), "+r"(x[8]), "+r"(x[9]), "+r"(x[10]), "+r"(x[11]), "+r"(x[12]), "+r"(x[13]), "+r"(x[14])
+        : "r"(y[0]), "r"(y[1]), "r"(y[2]), "r"(y[3]), "r"(y[4]), "r"(y[5]), "r"(y[6]), "r"(y[7]), "r"(y[8]), "r"(y[9]), "r"(y[10]), "r"(y[11]), "r"(y[12]), "r"(y[13]), "r"(y[14]));
+}
+
+template <>
+__device__ __forceinline__ void addc_chain<16>(uint32_t (&x)[16], const uint32_t (&y)[16]) {
+    asm("add.cc.u32 %0, %0, %16;\n\t"
+        "addc.cc.u32 %1, %1, %17;\n\t"
+        "addc.cc.u32 %2, %2, %18;\n\t"
+        "addc.cc.u32 %3, %3, %19;\n\t"
+        "addc.cc.u32 %4, %4, %20;\n\t"
+        "addc.cc.u32 %5, %5, %21;\n\t"
+        "addc.cc.u32 %6, %6, %22;\n\t"
+        "addc.cc.u32 %7, %7, %23;\n\t"
+        "addc.cc.u32 %8, %8, %24;\n\t"
+        "addc.cc.u32 %9, %9, %25;\n\t"
+        "addc.cc.u32 %10, %10, %26;\n\t"
+        "addc.cc.u32 %11, %11, %27;\n\t"
+        "addc.cc.u32 %12, %12, %28;\n\t"
+        "addc.cc.u32 %13, %13, %29;\n\t"
+        "addc.cc.u32 %14, %14, %30;\n\t"
+        "addc.u32 %15, %15, %31;"
+        : "+r"(x[0]), "+r"(x[1]), "+r"(x[2]), "+r"(x[3]), "+r"(x[4]), "+r"(x[5]), "+r"(x[6]), "+r"(x[7]), "+r"(x[8]), "+r"(x[9]), "+r"(x[10]), "+r"(x[11]), "+r"(x[12]), "+r"(x[13]), "+r"(x[14]), "+r"(x[15])
+        : "r"(y[0]), "r"(y[1]), "r"(y[2]), "r"(y[3]), "r"(y[4]), "r"(y[5]), "r"(y[6]), "r"(y[7]), "r"(y[8]), "r"(y[9]), "r"(y[10]), "r"(y[11]), "r"(y[12]), "r"(y[13]), "r"(y[14]), "r"(y[15]));
 }
 
 // r = x * m (mod 2^(32 CL)), two's complement x, unsigned 64-bit m

@@ -81,16 +81,22 @@ __device__ __forceinline__ uint64_t wtop64(const uint32_t (&x)[NL]) {
     return ((uint64_t)x[NL - 1] << 32) | x[NL - 2];
 }
 
+// -x mod 2^F (= ~x + 1; one single-statement carry chain, see addc_chain)
 template <int NL>
-__device__ __forceinline__ uint64_t wtop64_neg(const uint32_t (&x)[NL]) {
-    // top 64 bits of (-x mod 2^F)
-    uint32_t y[NL];
-    uint32_t borrow_in;
-    asm("sub.cc.u32 %0, 0, %1;" : "=r"(y[0]) : "r"(x[0]));
+__device__ __forceinline__ void wneg(uint32_t (&y)[NL], const uint32_t (&x)[NL]) {
+    uint32_t one[NL];
 #pragma unroll
-    for (int l = 1; l < NL; l++) asm("subc.cc.u32 %0, 0, %1;" : "=r"(y[l]) : "r"(x[l]));
-    asm("subc.u32 %0, 0, 0;" : "=r"(borrow_in));
-    (void)borrow_in;
+    for (int l = 0; l < NL; l++) {
+        y[l] = ~x[l];
+        one[l] = l == 0;
+    }
+    addc_chain<NL>(y, one);
+}
+
+template <int NL>
+__device__ __forceinline__ uint64_t wtop64_neg(const uint32_t (&x)[NL]) {  // top 64 bits of -x mod 2^F
+    uint32_t y[NL];
+    wneg<NL>(y, x);
     return ((uint64_t)y[NL - 1] << 32) | y[NL - 2];
 }
 
@@ -547,14 +553,12 @@ __global__ void __launch_bounds__(128) phase3_wide_kernel(WideDev w, int split, 
                         if (hit) {
                             if (pos < app_cap) {
                                 // v = V - (window - 1); dist = min(v, 2^F - v), floored to 2^-64
-                                uint32_t v[NL], nv[NL];
-                                asm("sub.cc.u32 %0, %1, %2;" : "=r"(v[0]) : "r"(e[0][0]), "r"(wm1[0]));
+                                uint32_t v[NL], nv[NL], mw[NL];
+                                wneg<NL>(mw, wm1);
 #pragma unroll
-                                for (int q = 1; q < NL; q++)
-                                    asm("subc.cc.u32 %0, %1, %2;" : "=r"(v[q]) : "r"(e[0][q]), "r"(wm1[q]));
-                                asm("sub.cc.u32 %0, 0, %1;" : "=r"(nv[0]) : "r"(v[0]));
-#pragma unroll
-                                for (int q = 1; q < NL; q++) asm("subc.cc.u32 %0, 0, %1;" : "=r"(nv[q]) : "r"(v[q]));
+                                for (int q = 0; q < NL; q++) v[q] = e[0][q];
+                                addc_chain<NL>(v, mw);
+                                wneg<NL>(nv, v);
                                 bool vzero = true;
 #pragma unroll
                                 for (int q = 0; q < NL; q++) vzero = vzero && v[q] == 0;
