@@ -100,52 +100,81 @@ __device__ __forceinline__ uint64_t wtop64_neg(const uint32_t (&x)[NL]) {  // to
     return ((uint64_t)y[NL - 1] << 32) | y[NL - 2];
 }
 
-// C(x, k) for x < 2^16, k <= 8: exact (< 2^128)
-__device__ __forceinline__ u128 binom_u128(uint64_t x, int k) {
-    u128 c = 1;
-    for (int r = 0; r < k; r++) {
-        if (x < (uint64_t)r + 1) return 0;
-        c = c * (u128)(x - r) / (u128)(r + 1);
+// x / k for k in 1..8 when k divides x exactly: shift out the power of two,
+// multiply by the inverse of the odd part mod 2^128 (no 128-bit division)
+__device__ __forceinline__ u128 exact_div_small(u128 x, int k) {
+    const u128 INV3 = ((u128)0xAAAAAAAAAAAAAAAAull << 64) | 0xAAAAAAAAAAAAAAABull;
+    const u128 INV5 = ((u128)0xCCCCCCCCCCCCCCCCull << 64) | 0xCCCCCCCCCCCCCCCDull;
+    const u128 INV7 = ((u128)0xB6DB6DB6DB6DB6DBull << 64) | 0x6DB6DB6DB6DB6DB7ull;
+    switch (k) {
+        case 2: return x >> 1;
+        case 3: return x * INV3;
+        case 4: return x >> 2;
+        case 5: return x * INV5;
+        case 6: return (x >> 1) * INV3;
+        case 7: return x * INV7;
+        case 8: return x >> 3;
+        default: return x;
     }
-    return c;
 }
 
-// C(x, k) for x < 512, k <= 8: exact (< 2^53)
-__device__ __forceinline__ uint64_t binom_u64(uint64_t x, int k) {
-    uint64_t c = 1;
-    for (int r = 0; r < k; r++) {
-        if (x < (uint64_t)r + 1) return 0;
-        c = c * (x - r) / (uint64_t)(r + 1);
+// bn[k] = C(x, k), k = 0..K, for x < 2^16 (every value < 2^128), exactly
+template <int K>
+__device__ __forceinline__ void binoms_u128(uint64_t x, u128 (&bn)[K + 1]) {
+    bn[0] = 1;
+#pragma unroll
+    for (int k = 1; k <= K; k++)
+        bn[k] = x + 1 < (uint64_t)k ? (u128)0 : exact_div_small(bn[k - 1] * (u128)(x + 1 - k), k);
+}
+
+__device__ __forceinline__ uint64_t exact_div_small64(uint64_t x, int k) {  // as exact_div_small, mod 2^64
+    switch (k) {
+        case 2: return x >> 1;
+        case 3: return x * 0xAAAAAAAAAAAAAAABull;
+        case 4: return x >> 2;
+        case 5: return x * 0xCCCCCCCCCCCCCCCDull;
+        case 6: return (x >> 1) * 0xAAAAAAAAAAAAAAABull;
+        case 7: return x * 0x6DB6DB6DB6DB6DB7ull;
+        case 8: return x >> 3;
+        default: return x;
     }
-    return c;
+}
+
+// bn[k] = C(x, k), k = 0..K, for x < 512 (every value < 2^53)
+template <int K>
+__device__ __forceinline__ void binoms_u64(uint64_t x, uint64_t (&bn)[K + 1]) {
+    bn[0] = 1;
+#pragma unroll
+    for (int k = 1; k <= K; k++) bn[k] = x + 1 < (uint64_t)k ? 0 : exact_div_small64(bn[k - 1] * (x + 1 - k), k);
 }
 
 // C(x, k) mod 2^(32 NL) for x < 2^32, k <= 8, computed exactly in 9 words
+// (the divisor of each step is a compile-time constant once unrolled)
 template <int NL>
 __device__ void binom_big(uint64_t x, int k, uint32_t (&out)[NL]) {
     uint32_t c[9] = {1, 0, 0, 0, 0, 0, 0, 0, 0};
-    for (int r = 0; r < k; r++) {
-        const uint64_t f = x - (uint64_t)r;
-        if (x < (uint64_t)r + 1) {
 #pragma unroll
-            for (int l = 0; l < NL; l++) out[l] = 0;
-            return;
-        }
-        // c *= f (f < 2^32)
-        uint64_t carry = 0;
+    for (int r = 0; r < 8; r++) {
+        if (r < k) {
+            if (x < (uint64_t)r + 1) {
 #pragma unroll
-        for (int l = 0; l < 9; l++) {
-            const uint64_t p = (uint64_t)c[l] * f + carry;
-            c[l] = (uint32_t)p;
-            carry = p >> 32;
-        }
-        // c /= r + 1 (exact)
-        uint64_t rem = 0;
+                for (int l = 0; l < 9; l++) c[l] = 0;
+            }
+            const uint64_t f = x - (uint64_t)r;
+            uint64_t carry = 0;
 #pragma unroll
-        for (int l = 8; l >= 0; l--) {
-            const uint64_t cur = (rem << 32) | c[l];
-            c[l] = (uint32_t)(cur / (uint64_t)(r + 1));
-            rem = cur % (uint64_t)(r + 1);
+            for (int l = 0; l < 9; l++) {
+                const uint64_t p = (uint64_t)c[l] * f + carry;
+                c[l] = (uint32_t)p;
+                carry = p >> 32;
+            }
+            uint64_t rem = 0;
+#pragma unroll
+            for (int l = 8; l >= 0; l--) {
+                const uint64_t cur = (rem << 32) | c[l];
+                c[l] = (uint32_t)(cur / (uint64_t)(r + 1));
+                rem = cur % (uint64_t)(r + 1);
+            }
         }
     }
 #pragma unroll
@@ -159,39 +188,50 @@ __device__ __forceinline__ void wload(uint32_t (&x)[NL], const uint32_t* p, int6
 }
 
 // ---------------------------------------------------------------- seeds
+// one 64-thread block per tile (grid-stride): threads 0..D compute
+// C(i0, k) exactly once per tile, then thread c < ncoef forms column entry c
 template <int NL>
-__global__ void wseed_kernel(WideDev w, const uint64_t* tile_base, uint32_t* seeds) {
-    const uint64_t total = tile_base[w.g.S] * (uint64_t)w.ncoef;
-    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < total;
-         k += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t gt = k / (uint64_t)w.ncoef;
-        const int c = (int)(k - gt * (uint64_t)w.ncoef);
-        int j = 0;
-        while (wcol(w.D, j + 1, 0) <= c) j++;
-        const int l = c - wcol(w.D, j, 0);
+__global__ void __launch_bounds__(64) wseed_kernel(WideDev w, const uint64_t* tile_base, uint32_t* seeds) {
+    __shared__ uint32_t bn[WMAXD + 1][NL];
+    const uint64_t tiles = tile_base[w.g.S];
+    const int c = threadIdx.x;
+    int j = 0;
+    while (j < w.D && wcol(w.D, j + 1, 0) <= c) j++;
+    const int l = c - wcol(w.D, j, 0);
+    for (uint64_t gt = blockIdx.x; gt < tiles; gt += gridDim.x) {
         const int64_t t = locate_super(tile_base, w.g.S, gt);
         const uint64_t i0 = (gt - tile_base[t]) * TILE;
-        uint32_t acc[NL];
+        __syncthreads();  // the previous tile's binomials are consumed
+        if (c <= w.D) {
+            uint32_t b[NL];
+            binom_big<NL>(i0, c, b);
 #pragma unroll
-        for (int q = 0; q < NL; q++) acc[q] = 0;
-        for (int m = l; m <= w.D - j; m++) {
-            uint32_t qv[NL], bn[NL];
-            wload<NL>(qv, w.coef + ((int64_t)wcol(w.D, j, m) * NL) * w.g.S + t, w.g.S);
-            binom_big<NL>(i0, m - l, bn);
-            // acc += qv * bn mod 2^F
+            for (int q = 0; q < NL; q++) bn[c][q] = b[q];
+        }
+        __syncthreads();
+        if (c < w.ncoef) {
+            uint32_t acc[NL];
 #pragma unroll
-            for (int h = 0; h < NL; h++) {
-                uint32_t carry = 0;
+            for (int q = 0; q < NL; q++) acc[q] = 0;
+            for (int m = l; m <= w.D - j; m++) {
+                uint32_t qv[NL];
+                wload<NL>(qv, w.coef + ((int64_t)wcol(w.D, j, m) * NL) * w.g.S + t, w.g.S);
+                // acc += qv * C(i0, m - l) mod 2^F
 #pragma unroll
-                for (int q = 0; q + h < NL; q++) {
-                    const uint64_t p = (uint64_t)qv[q] * bn[h] + acc[q + h] + carry;
-                    acc[q + h] = (uint32_t)p;
-                    carry = (uint32_t)(p >> 32);
+                for (int h = 0; h < NL; h++) {
+                    const uint32_t bh = bn[m - l][h];
+                    uint32_t carry = 0;
+#pragma unroll
+                    for (int q = 0; q + h < NL; q++) {
+                        const uint64_t p = (uint64_t)qv[q] * bh + acc[q + h] + carry;
+                        acc[q + h] = (uint32_t)p;
+                        carry = (uint32_t)(p >> 32);
+                    }
                 }
             }
-        }
 #pragma unroll
-        for (int q = 0; q < NL; q++) seeds[k * NL + q] = acc[q];
+            for (int q = 0; q < NL; q++) seeds[(gt * w.ncoef + c) * NL + q] = acc[q];
+        }
     }
 }
 
@@ -236,8 +276,7 @@ __device__ __forceinline__ void wwalk_packet(const uint32_t* tcol, int lane, uin
     uint32_t c[E][NL];
     const uint64_t off = (uint64_t)WPKT * lane;
     uint64_t bn[E];
-#pragma unroll
-    for (int k = 0; k < E; k++) bn[k] = binom_u64(off, k);
+    binoms_u64<E - 1>(off, bn);
 #pragma unroll
     for (int l = 0; l < E; l++) {
 #pragma unroll
@@ -328,8 +367,7 @@ __device__ __forceinline__ void wdomain_poly(const WideDev& w, const uint64_t* t
     const uint64_t di = i % TILE;
     const uint32_t* col = w.seeds + gt * w.ncoef * NL;
     uint64_t bn[D + 1];
-#pragma unroll
-    for (int k = 0; k <= D; k++) bn[k] = binom_u64(di, k);
+    binoms_u64<D>(di, bn);
 #pragma unroll
     for (int j = 0; j <= D; j++) {
         uint32_t acc[NL];
@@ -365,13 +403,12 @@ struct WSubSrc {  // the lane's subdomains, shifted from its domain polynomial
             s0[q] = sc[q];
             s1[q] = sc[NL + q];
         }
-        u128 bn = 1;  // C(start, k - 1), rolling
+        u128 bn[D + 1];
+        binoms_u128<D>(start, bn);
 #pragma unroll
         for (int k2 = 1; k2 <= D; k2++) {
-            const u128 b1 = bn;                                            // C(start, k2 - 1)
-            bn = start < (uint64_t)k2 ? 0 : bn * (u128)(start - k2 + 1) / (u128)k2;  // C(start, k2)
-            wmad128<NL>(s0, sc + k2 * NL, bn);
-            if (k2 >= 2) wmad128<NL>(s1, sc + k2 * NL, b1);
+            wmad128<NL>(s0, sc + k2 * NL, bn[k2]);                  // s_k2 C(start, k2)
+            if (k2 >= 2) wmad128<NL>(s1, sc + k2 * NL, bn[k2 - 1]);  // s_k2 C(start, k2 - 1)
         }
         const uint64_t pad = last ? pad_last : pad_full;
         a = wtop64_neg<NL>(s1);
@@ -437,8 +474,7 @@ template <int D, int NL>
 __device__ __forceinline__ void wcolumn_at(const uint32_t* sc, uint64_t x0, uint32_t (&c)[D + 1][NL]) {
     // Delta^l P(x0) = sum_{k >= l} s_k C(x0, k - l)
     u128 bn[D + 1];
-#pragma unroll
-    for (int k = 0; k <= D; k++) bn[k] = binom_u128(x0, k);
+    binoms_u128<D>(x0, bn);
 #pragma unroll
     for (int l = 0; l <= D; l++) {
 #pragma unroll
@@ -605,7 +641,9 @@ __global__ void __launch_bounds__(128) wtabdiff_kernel(WideDev w, const uint64_t
             uint32_t c[WMAXD + 1][NL];
             for (int l = 0; l < E; l++) {
                 for (int q = 0; q < NL; q++) c[l][q] = __ldg(&tcol[(wcol(D, j, l)) * NL + q]);
-                for (int k = 1; l + k < E; k++) wmad64<NL>(c[l], tcol + wcol(D, j, l + k) * NL, binom_u64(off, k));
+                uint64_t bo[WMAXD + 1];
+                binoms_u64<WMAXD>(off, bo);
+                for (int k = 1; l + k < E; k++) wmad64<NL>(c[l], tcol + wcol(D, j, l + k) * NL, bo[k]);
             }
             for (int k = 0; k < WPKT; k++) {
                 const uint64_t i = tile * TILE + off + k;
@@ -686,7 +724,7 @@ int run_wslice_locked(Workspace& ws, WideWs& wws, const hrb_wslice* s, int algo,
     w.seeds = (const uint32_t*)wws.seeds.p;
     auto tb = (const uint64_t*)ws.tile_base.p;
 #define SEED(D_, NL_) \
-    wseed_kernel<NL_><<<sm_count() * 8, 256, 0, st>>>(w, tb, (uint32_t*)wws.seeds.p)
+    wseed_kernel<NL_><<<sm_count() * 16, 64, 0, st>>>(w, tb, (uint32_t*)wws.seeds.p)
     HRB_WIDE_DISPATCH(w.D, SEED)
 #undef SEED
     CK(cudaGetLastError());
@@ -772,7 +810,7 @@ int wtabdiff_impl(Workspace& ws, WideWs& wws, const hrb_wslice* s, uint32_t* out
     if ((rc = wws.seeds.ensure(sizeof(uint32_t) * max_tiles * w.ncoef * w.NL))) return rc;
     w.seeds = (const uint32_t*)wws.seeds.p;
     auto tb = (const uint64_t*)ws.tile_base.p;
-#define SEED(D_, NL_) wseed_kernel<NL_><<<sm_count() * 8, 256, 0, st>>>(w, tb, (uint32_t*)wws.seeds.p)
+#define SEED(D_, NL_) wseed_kernel<NL_><<<sm_count() * 16, 64, 0, st>>>(w, tb, (uint32_t*)wws.seeds.p)
     HRB_WIDE_DISPATCH(w.D, SEED)
 #undef SEED
 #define TABW(D_, NL_) wtabdiff_kernel<D_, NL_><<<sm_count() * 4, 128, 0, st>>>(w, tb, s->n_total, out)
