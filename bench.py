@@ -57,6 +57,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-e2e-full", action="store_true", help="skip the run_range end-to-end measurement")
+    ap.add_argument("--wide-delta", type=int, default=4, help="also measure the high-degree path (0: skip)")
     return ap.parse_args()
 
 
@@ -122,7 +123,65 @@ def e2e_full(args, batch, workers, dist):
             "interval_args": interval, "workers": workers,
             "phase_wall_ms": {k: round(v, 3) for k, v in rows.items()},
             "host_generation": "native (libhrbhost.so)" if batch.supers.__class__.__name__ == "PackedSupers"
-            else "python (mpmath)"}
+            else "python (mpmath)", "_records": out.records}
+
+
+def wide_run(args, batch, workers, dist, want_records):
+    """The high-degree path (delta_R = --wide-delta, one Taylor model per
+    2^33..2^40 arguments; an extension of the reference, wide.py) over the
+    rank's range: the device step with inputs resident (hrb_wrun_slice, CUDA
+    events, L2 flushed), and run_range(wide=...) end to end (wall clock:
+    host models, upload, phases, download, confirmation).  Its records must
+    equal the delta = 2 run's."""
+    import torch
+
+    from paper_1211_3056_b200.funnel import run_range
+    from paper_1211_3056_b200.wide import WideDeviceSlice, WideGenConfig, WideRunner, prepare_wide
+
+    cfg = make_cfg(args)
+    w = WideGenConfig.for_degree(args.wide_delta, N=1 << args.log2_N)
+    start, count = int(batch.m0[0]), batch.arguments
+    t0 = time.perf_counter()
+    wb = prepare_wide(args.fn, 0, start, count, cfg.fmt, w, workers=workers)
+    host_s = time.perf_counter() - t0
+    ds = WideDeviceSlice(wb)
+    runner = WideRunner(ds, 2, 8, sub_cap=max(1 << 16, wb.n_total // 4), cand_cap=1 << 20)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream()
+    for _ in range(max(3, args.warmup)):
+        runner.launch()
+    torch.cuda.synchronize()
+    ms = []
+    for _ in range(args.steps):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        runner.launch()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    counts = [int(x) for x in runner.counts_host()[:3]]
+    del runner, ds, flush
+    interval = 1 << min(args.log2_args, 40)
+    run = lambda: run_range(args.fn, 0, start, count, cfg, interval_args=interval, workers=workers,  # noqa: E731
+                            wide=w)
+    out = run()
+    ts = []
+    for _ in range(3):
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        out = run()
+        torch.cuda.synchronize()
+        ts.append(time.perf_counter() - t1)
+    same = [(r.argument, r.distance.raw, r.domain_id) for r in out.records] == \
+        [(r.argument, r.distance.raw, r.domain_id) for r in want_records] if want_records is not None else None
+    return {"delta": w.delta, "frac_bits": w.frac_bits, "super_args": w.tau * w.N, "super_domains": wb.n_super,
+            "host_model_s": host_s, "device_ms": float(np.mean(ms)), "counts": counts,
+            "e2e_full_s": float(np.median(ts)), "records": len(out.records), "records_equal_delta2": same,
+            "parity": "records pinned (reference exhaustive enumerator, delta=2 records); tabulated values and "
+                      "phase flags parity-unpinned: the reference rejects delta >= 3 (polygen.py:81-82)"}
 
 
 def workload_name(args):
@@ -416,6 +475,11 @@ def main():
     full = None
     if not args.no_e2e_full:
         full = e2e_full(args, batch, workers, dist)
+    wide = None
+    if args.wide_delta:
+        wide = wide_run(args, batch, workers, dist, full["_records"] if full else None)
+    if full:
+        full.pop("_records")
     # ---- end of run: NCCL gather of the per-rank counters and candidate lists
     from paper_1211_3056_b200.fpformat import index_bits
     from paper_1211_3056_b200.shard import ShardResult, gather_shards
@@ -427,7 +491,8 @@ def main():
                     dtype=np.uint64).reshape(-1, 4)
     local_res = ShardResult(np.array([counts[0], counts[1], counts[2], 0, counts[3], count], dtype=np.int64), cand)
     t_all = torch.tensor([ms, float(np.median(p1_ms)), e2e["ms_per_step"] if e2e else 0.0,
-                          full["seconds"] if full else 0.0], device="cpu" if one_dev else "cuda")
+                          full["seconds"] if full else 0.0, wide["device_ms"] if wide else 0.0,
+                          wide["e2e_full_s"] if wide else 0.0], device="cpu" if one_dev else "cuda")
     gather_ms = 0.0
     if dist:
         dist.all_reduce(t_all, op=dist.ReduceOp.MAX)
@@ -437,7 +502,7 @@ def main():
         gather_ms = 1e3 * (time.perf_counter() - tg)
     else:
         merged, per_rank = local_res, local_res.counters[None, :]
-    ms_max, p1_max, e2e_max, full_max = (float(x) for x in t_all.cpu())
+    ms_max, p1_max, e2e_max, full_max, wide_ms, wide_full = (float(x) for x in t_all.cpu())
     if rank != 0:
         dist.destroy_process_group()
         return
@@ -450,6 +515,11 @@ def main():
         full["seconds"] = full_max
         full["value"] = total_args / full_max
         full["unit"] = UNIT
+    if wide:
+        wide["device_ms"], wide["e2e_full_s"] = wide_ms, wide_full
+        wide["value"] = total_args / (wide_ms / 1e3)
+        wide["e2e_full_value"] = total_args / wide_full
+        wide["unit"] = UNIT
     clocks = sampler.summary()
     # ---- roofline of the dominant kernel (phase 1): INT-pipe bound
     peak = int_peak()
@@ -503,7 +573,7 @@ def main():
             "clocks": clocks, "gpu_launches": KERNELS_PER_STEP * args.steps, "roofline": roofline,
             "host_polygen": {"seconds": prep_s, "workers": workers, "super_domains": batch.n_super,
                              "args_per_s": count / prep_s},
-            "e2e": e2e, "e2e_full": full}
+            "e2e": e2e, "e2e_full": full, "wide": wide}
     if not args.no_cpu_baseline and world == 1:  # rank 0 at N=1 only
         cb = cpu_baseline(args, batch, args.cpu_seconds)
         cb["counts_match_gpu"] = cb.pop("counts") == [int(counts[0]), int(counts[1]), int(counts[2])]

@@ -358,7 +358,7 @@ MANIFEST_VERSION = 2  # bump when the interval-line format or the results of a c
 
 
 def manifest_key(fn: str, binade: int, start: int, count: int, cfg: PipelineConfig, interval_args: int,
-                 confirm: bool = True) -> str:
+                 confirm: bool = True, wide=None) -> str:
     """Hash of everything that determines a run's results.  The host worker
     count (PhaseConfig.parallel_width) does not change results, so it is
     normalised out: a run may resume on a machine with other core counts."""
@@ -366,7 +366,7 @@ def manifest_key(fn: str, binade: int, start: int, count: int, cfg: PipelineConf
     import hashlib
 
     norm = dataclasses.replace(cfg, phase=dataclasses.replace(cfg.phase, parallel_width=1))
-    ident = (MANIFEST_VERSION, fn, binade, start, count, norm, interval_args, confirm)
+    ident = (MANIFEST_VERSION, fn, binade, start, count, norm, interval_args, confirm) + ((wide,) if wide else ())
     return hashlib.sha256(repr(ident).encode()).hexdigest()[:32]
 
 
@@ -427,9 +427,34 @@ def read_manifest(path: str, key: str) -> dict:
     return done
 
 
+def execute_wide(batch, cfg: PipelineConfig, algo: str, fn: str | None = None, confirm: bool = True,
+                 workers: int | None = None) -> SliceOutput:
+    """A high-degree slice (wide.WideSliceBatch) through ONE host-buffer ABI
+    call (hrb_wrun_slice_host), then the rigorous confirmation; statistics
+    as execute_batch_host.  The wide kernels run the regular family."""
+    from .wide import candidates_of, run_wide_host
+
+    if algo not in ("regular", "regular_unrolled"):
+        raise ValueError("high-degree slices run the regular search family")
+    res = run_wide_host(batch, ALGO_CODE[Algorithm(algo)], cfg.phase.phase2_split)
+    n_fail, n_sub, n_cand, iters, a2, a3 = (int(x) for x in res.counts)
+    stats = PhaseStats()
+    stats.rows.append(PhaseRow("phase1", batch.n_total, n_fail, batch.arguments, res.device_ms))
+    stats.rows.append(PhaseRow("phase2", n_fail, n_sub, a2, 0.0))
+    cand = candidates_of(batch, res)
+    stats.rows.append(PhaseRow("phase3", n_sub, n_cand, a3, 0.0))
+    records = []
+    t4 = time.perf_counter()
+    if confirm:
+        records = confirm_candidates(fn or cfg.fn, cand, cfg.fmt, workers if workers is not None else
+                                     cfg.phase.parallel_width)
+    stats.rows.append(PhaseRow("confirm", len(cand), len(records), len(cand), (time.perf_counter() - t4) * 1e3))
+    return SliceOutput(batch, None, None, cand, records, stats, iters)
+
+
 def run_range(fn: str, binade: int, start: int, count: int, cfg: PipelineConfig, interval_args: int = 1 << 36,
               workers: int | None = None, confirm: bool = True, manifest: str | None = None,
-              native: bool | None = None) -> RangeOutput:
+              native: bool | None = None, wide=None) -> RangeOutput:
     """A long argument range as consecutive intervals, the way the paper walks
     a binade: the block schedule of the WHOLE range is
     planned once (so blocks, domain ids and results are exactly those of a
@@ -439,14 +464,24 @@ def run_range(fn: str, binade: int, start: int, count: int, cfg: PipelineConfig,
     pipeline.py:187-197).  The host Taylor generation of interval i+1 runs in
     a background thread while the device and the host confirmation work on
     interval i.  manifest: a path that makes the run resumable (see
-    read_manifest); finished intervals are restored, not recomputed."""
+    read_manifest); finished intervals are restored, not recomputed.
+    wide: a wide.WideGenConfig switches to the high-degree path (delta_R
+    3..8, one Taylor model per large super-domain; the regular family; an
+    extension of the reference, see wide.py) -- same records."""
     from concurrent.futures import ThreadPoolExecutor
 
     from .shard import partition_blocks
     from .slices import pack_plan, plan_arrays
 
     w = workers if workers is not None else cfg.phase.parallel_width
-    plan = plan_arrays(fn, binade, cfg.fmt, cfg.polygen, start, count)
+    if wide is not None:
+        from .wide import pack_wide, plan_wide
+
+        if cfg.phase.algorithm == "lefevre":
+            raise ValueError("high-degree slices run the regular search family")
+        plan = plan_wide(fn, binade, cfg.fmt, wide, start, count)
+    else:
+        plan = plan_arrays(fn, binade, cfg.fmt, cfg.polygen, start, count)
     sizes = plan.sizes
     n_int = max(1, -(-int(sizes.sum()) // max(1, interval_args)))
     parts = [p for p in partition_blocks(sizes, n_int) if p[1] > p[0]]
@@ -454,6 +489,8 @@ def run_range(fn: str, binade: int, start: int, count: int, cfg: PipelineConfig,
     bstart_of = [int(plan.bstart[p[0]]) for p in parts]
 
     def prepare(part):
+        if wide is not None:
+            return pack_wide(plan[part[0]:part[1]], wide, w)
         return pack_plan(plan[part[0]:part[1]], cfg.word_bits, budget_ceiling=ceiling, workers=w, native=native)
 
     done, sink = {}, None
@@ -461,7 +498,7 @@ def run_range(fn: str, binade: int, start: int, count: int, cfg: PipelineConfig,
         import json
         import os
 
-        key = manifest_key(fn, binade, start, count, cfg, interval_args, confirm)
+        key = manifest_key(fn, binade, start, count, cfg, interval_args, confirm, wide)
         done = read_manifest(manifest, key)
         # no valid header (absent, empty, or torn by a crash before its
         # newline was durable): start the file over
@@ -500,8 +537,11 @@ def run_range(fn: str, binade: int, start: int, count: int, cfg: PipelineConfig,
                     futs[todo[i + 1]] = ex.submit(prepare, parts[todo[i + 1]])
                 algo = cfg.phase.algorithm
                 if algo == "auto":
-                    algo = select_algorithm(prev)
-                out = execute_batch_host(batch, cfg, algo, fn, confirm=confirm, workers=w)
+                    algo = select_algorithm(prev) if wide is None else "regular"
+                if wide is not None:
+                    out = execute_wide(batch, cfg, algo, fn, confirm=confirm, workers=w)
+                else:
+                    out = execute_batch_host(batch, cfg, algo, fn, confirm=confirm, workers=w)
                 out.stats.algorithm_choices.append((bstart_of[k], algo))
                 records.extend(out.records)
                 stats_list.append(out.stats)
