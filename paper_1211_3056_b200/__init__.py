@@ -83,28 +83,41 @@ __version__ = "0.1.0"
 
 
 def domain_coefficient_sets(r_polys, cfg: PolyGenConfig) -> list[tuple]:
-    """Per-domain coefficient tuples (s_0..s_delta) of one super-domain
-    (polygen.py:274-280), walked on the GPU (hrb_domain_coefficients)."""
-    from .device import DeviceSlice, domain_coefficients
-    from .arith import as_int
+    """Drop-in for the reference's domain_coefficient_sets (polygen.py:274-280):
+    per-domain coefficient tuples (s_0..s_delta) = (r_0(i), .., r_delta(i))
+    of one super-domain, i < cfg.tau, as MPInt with cfg.limbs limbs -- the
+    values of the reference's (j, u, i) packet walk (generate_packets,
+    polygen.py:255-271).  The walk runs on the GPU (hrb_domain_coefficients:
+    add-with-carry chains over L+1 two's-complement limbs, exact while the
+    values fit the MPInt budget).  Where the reference's walk would raise
+    MPOverflowError (fixedpoint.py:136), the exact host replay raises it
+    first; only the walk is involved (FpFormat, eps and the search do not
+    enter), so the slice is packed without the phase checks."""
     from fractions import Fraction
 
-    sd = SuperDomain(0, cfg.tau * cfg.N, cfg.N, cfg.tau, cfg.mu, cfg.nu, 0, 0, tuple(r_polys), Fraction(0))
-    pg = PolyGenConfig(tau=cfg.tau, N=cfg.N, mu=cfg.mu, nu=cfg.nu, delta=2, limbs=cfg.limbs,
-                       frac_bits=max(cfg.frac_bits, 64), guard=cfg.guard)
-    padded = list(r_polys) + [BinomialPoly((0,))] * (3 - len(r_polys))
-    batch = pack_slice([SuperDomain(0, sd.count, sd.n_p, sd.tau, sd.mu, sd.nu, 0, 0, tuple(padded), Fraction(0))],
-                       FpFormat(53, 32), pg, 64, 0, check=False)
-    from .slices import _walk_bound, _emulate_walk
+    from .arith import as_int
+    from .device import DeviceSlice, domain_coefficients
+    from .slices import _emulate_walk, _walk_bound
 
-    if _walk_bound(sd) >> (32 * cfg.limbs):
-        _emulate_walk(sd, cfg.limbs)
+    r_polys = [BinomialPoly(tuple(as_int(c) for c in rp.coeffs), rp.scale) for rp in r_polys]
+    delta = len(r_polys) - 1
+    if not 0 <= delta <= 2:
+        raise ValueError("the device walk takes delta <= 2 (the reference's PolyGenConfig range)")
+    sd = SuperDomain(0, cfg.tau * cfg.N, cfg.N, cfg.tau, cfg.mu, cfg.nu, 0, 0, tuple(r_polys), Fraction(0))
+    if _walk_bound(sd) >> (32 * cfg.limbs) or (cfg.tau * cfg.tau) >> (32 * cfg.limbs):
+        _emulate_walk(sd, cfg.limbs)  # raises MPOverflowError where the reference's walk would
+    padded = tuple(r_polys) + (BinomialPoly((0,)),) * (2 - delta)
+    # frac_bits / word_bits only feed the search; any legal pair packs the walk
+    pg = PolyGenConfig(tau=cfg.tau, N=cfg.N, mu=cfg.mu, nu=cfg.nu, delta=2, limbs=cfg.limbs, frac_bits=64,
+                       guard=cfg.guard)
+    batch = pack_slice([SuperDomain(0, sd.count, sd.n_p, sd.tau, sd.mu, sd.nu, 0, 0, padded, Fraction(0))],
+                       FpFormat(53, 32), pg, 64, 0, check=False)
     raw = domain_coefficients(DeviceSlice(batch))
     cl = raw.shape[1]
     out = []
     for i in range(cfg.tau):
         vals = []
-        for j in range(len(r_polys)):
+        for j in range(delta + 1):
             v = 0
             for l in range(cl):
                 v |= int(raw[j, l, i]) << (32 * l)

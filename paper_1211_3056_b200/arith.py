@@ -136,9 +136,12 @@ class MPInt:
         self._n = len(limbs)
 
     @classmethod
-    def _raw(cls, value: int, n: int) -> "MPInt":
+    def _raw(cls, value: int, n: int, what: str | None = None) -> "MPInt":
+        # the reference's messages: from_int "<v> needs <b> bits, have <B>",
+        # mp_add "addition carry out of top limb", mp_mul "product exceeds
+        # limb budget" (fixedpoint.py:136-137, 239, 291, 300)
         if abs(value) >> (LIMB_BITS * n):
-            raise MPOverflowError(f"{value} needs {abs(value).bit_length()} bits, have {LIMB_BITS * n}")
+            raise MPOverflowError(what or f"{value} needs {abs(value).bit_length()} bits, have {LIMB_BITS * n}")
         obj = cls.__new__(cls)
         obj._v = value
         obj._n = n
@@ -176,23 +179,26 @@ class MPInt:
     def __neg__(self) -> "MPInt":
         return MPInt._raw(-self._v, self._n)
 
+    _ADD = "addition carry out of top limb"
+    _MUL = "product exceeds limb budget"
+
     def __add__(self, other):
         o = self._other(other)
-        return NotImplemented if o is NotImplemented else MPInt._raw(self._v + o, self._n)
+        return NotImplemented if o is NotImplemented else MPInt._raw(self._v + o, self._n, self._ADD)
 
     __radd__ = __add__
 
     def __sub__(self, other):
         o = self._other(other)
-        return NotImplemented if o is NotImplemented else MPInt._raw(self._v - o, self._n)
+        return NotImplemented if o is NotImplemented else MPInt._raw(self._v - o, self._n, self._ADD)
 
     def __rsub__(self, other):
         o = self._other(other)
-        return NotImplemented if o is NotImplemented else MPInt._raw(o - self._v, self._n)
+        return NotImplemented if o is NotImplemented else MPInt._raw(o - self._v, self._n, self._ADD)
 
     def __mul__(self, other):
         o = self._other(other)
-        return NotImplemented if o is NotImplemented else MPInt._raw(self._v * o, self._n)
+        return NotImplemented if o is NotImplemented else MPInt._raw(self._v * o, self._n, self._MUL)
 
     __rmul__ = __mul__
 

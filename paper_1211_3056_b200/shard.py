@@ -131,18 +131,16 @@ def merge_shards(parts: Sequence[ShardResult]) -> ShardResult:
                        np.concatenate([p.records for p in parts], axis=0))
 
 
-def _run_rank(blocks, rank, world, fn, binade, cfg, algo, workers, confirm) -> ShardResult:
+def _run_rank(plan, rank, world, fn, binade, cfg, algo, workers, confirm) -> ShardResult:
     from .funnel import _resolve, execute_batch
-    from .slices import pack_slice, supers_of_blocks
+    from .slices import pack_plan
 
-    b0, b1 = partition_blocks([b.bcount for b in blocks], world)[rank]
-    mine = blocks[b0:b1]
-    if not mine:
+    b0, b1 = partition_blocks(plan.sizes, world)[rank]
+    if b1 <= b0:
         return ShardResult(np.zeros(N_COUNTERS, np.int64))
-    supers = supers_of_blocks(mine, workers)
     ceiling = cfg.phase.budgets.eps_dprime if cfg.phase.budgets is not None else None
-    batch = pack_slice(supers, cfg.fmt, cfg.polygen, cfg.word_bits, binade, budget_ceiling=ceiling, workers=workers)
-    out = execute_batch(batch, cfg, _resolve(cfg, algo), fn, confirm=confirm)
+    batch = pack_plan(plan[b0:b1], cfg.word_bits, budget_ceiling=ceiling, workers=workers)
+    out = execute_batch(batch, cfg, _resolve(cfg, algo), fn, confirm=confirm, workers=workers)
     return ShardResult.of(len(out.fail_global), len(out.sub_table[0]), out.candidates, out.records,
                           out.iterations, batch.arguments)
 
@@ -152,10 +150,10 @@ def run_logical_shards(fn: str, binade: int, start: int, count: int, cfg, world:
     """Single-GPU stand-in for a `world`-rank run: the same partition, the
     shards run one after another on the current device, merged in rank
     order (tests the shard boundaries without 8 GPUs)."""
-    from .slices import plan_blocks
+    from .slices import plan_arrays
 
-    blocks = plan_blocks(fn, binade, cfg.fmt, cfg.polygen, start, count)
-    parts = [_run_rank(blocks, r, world, fn, binade, cfg, algo, workers, confirm) for r in range(world)]
+    plan = plan_arrays(fn, binade, cfg.fmt, cfg.polygen, start, count)
+    parts = [_run_rank(plan, r, world, fn, binade, cfg, algo, workers, confirm) for r in range(world)]
     return merge_shards(parts), np.stack([p.counters for p in parts])
 
 
@@ -165,10 +163,10 @@ def run_sharded(fn: str, binade: int, start: int, count: int, cfg, algo: str | N
     ranks of `group`; this rank runs its contiguous share on the current
     CUDA device.  Returns (merged ShardResult, per-rank counters) on every
     rank; records are confirmed on the rank that found them."""
-    from .slices import plan_blocks
+    from .slices import plan_arrays
 
-    blocks = plan_blocks(fn, binade, cfg.fmt, cfg.polygen, start, count)
-    local = _run_rank(blocks, rank, world, fn, binade, cfg, algo, workers, confirm)
+    plan = plan_arrays(fn, binade, cfg.fmt, cfg.polygen, start, count)
+    local = _run_rank(plan, rank, world, fn, binade, cfg, algo, workers, confirm)
     if world == 1:
         return local, local.counters[None, :]
     return gather_shards(local, group)

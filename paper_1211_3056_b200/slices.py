@@ -543,7 +543,8 @@ def pack_plan(plan: BlockPlan, word_bits: int, budget_ceiling: Fraction | None =
     no budget ceiling) every block runs in C++ over `workers` host threads,
     bit-identical to the Python path; blocks it flags go through the exact
     Python path one by one (raising the reference's error where the
-    reference raises).  native=False forces the Python path."""
+    reference raises).  native=False forces the Python path; otherwise the
+    native path runs wherever it covers the configuration."""
     from . import hostgen
 
     fmt, pg = plan.fmt, plan.pg
@@ -552,7 +553,7 @@ def pack_plan(plan: BlockPlan, word_bits: int, budget_ceiling: Fraction | None =
         raise ValueError("empty slice")
     if not word_bits <= F <= 128:
         raise ValueError(f"the B200 path needs word_bits <= frac_bits <= 128 (got F={F}, W={word_bits})")
-    use_native = hostgen.covers(plan.fn, plan.binade, fmt, pg, budget_ceiling) if native is None else native
+    use_native = native is not False and hostgen.covers(plan.fn, plan.binade, fmt, pg, budget_ceiling)
     if not use_native:
         blocks = [plan.block(i) for i in range(len(plan))]
         return pack_slice(supers_of_blocks(blocks, workers), fmt, pg, word_bits, plan.binade,

@@ -12,6 +12,8 @@ Pins, in order of strength:
 - the Python host path (slices.pack_plan(native=False)) on random
   configurations.
 """
+import json
+import os
 import random
 from fractions import Fraction
 
@@ -129,3 +131,33 @@ def test_fallback_raises_like_the_reference():
         slices.pack_plan(plan, 64, workers=1, native=False)
     with pytest.raises(ValueError):
         slices.pack_plan(plan, 64, workers=1, native=True)
+
+
+def _overflow_cases():
+    with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "overflow.json")) as fh:
+        return json.load(fh)
+
+
+@pytest.mark.parametrize("native", [False, True])
+def test_limb_overflow_matches_reference(native):
+    """Where the reference's host generation raises MPOverflowError under a
+    tight limb budget (tests/golden/make_overflow.py: MPInt.from_int in
+    taylor_approx, MPInt products in hierarchical_split), this package's
+    planning + packing raises the same class with the same message, on
+    both the Python and the native path; where the reference succeeds, so
+    does this package, with the same number of domains."""
+    from paper_1211_3056_b200.arith import MPOverflowError
+
+    for c in _overflow_cases():
+        fmt = FpFormat(c["p"], c["eps_bits"])
+        pg = PolyGenConfig(tau=c["tau"], N=c["N"], mu=c["mu"], nu=c["nu"], delta=2, limbs=c["limbs"],
+                           frac_bits=c["frac_bits"], guard=32)
+        plan = slices.plan_arrays(c["fn"], c["binade"], fmt, pg, 0, 1 << (c["p"] - 1))
+        if c["ok"]:
+            b = slices.pack_plan(plan, 64 if c["frac_bits"] >= 64 else 32, workers=1, native=native)
+            assert b.n_total == c["tasks"], c
+        else:
+            assert c["error"] == "MPOverflowError"
+            with pytest.raises(MPOverflowError) as ei:
+                slices.pack_plan(plan, 64 if c["frac_bits"] >= 64 else 32, workers=1, native=native)
+            assert str(ei.value) == c["message"], c
