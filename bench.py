@@ -175,8 +175,7 @@ def wide_run(args, batch, workers, dist, want_records):
         out = run()
         torch.cuda.synchronize()
         ts.append(time.perf_counter() - t1)
-    same = [(r.argument, r.distance.raw, r.domain_id) for r in out.records] == \
-        [(r.argument, r.distance.raw, r.domain_id) for r in want_records] if want_records is not None else None
+    same = bool(out.records == want_records) if want_records is not None else None
     return {"delta": w.delta, "frac_bits": w.frac_bits, "super_args": w.tau * w.N, "super_domains": wb.n_super,
             "host_model_s": host_s, "device_ms": float(np.mean(ms)), "counts": counts,
             "e2e_full_s": float(np.median(ts)), "records": len(out.records), "records_equal_delta2": same,

@@ -27,6 +27,7 @@ from . import _native as nat
 from .arith import LIMB_BITS, MODE_CODE, DivisionMode, MPInt, UFrac, as_int
 from .enclosure import decide_hr
 from .fpformat import Domain, ErrorBudget, FpFormat, HrCaseRecord, bits_float, index_bits
+from .records import RecordSet
 from .search import ALGO_CODE, Algorithm
 from .slices import (SliceBatch, SuperDomain, build_super_domains, check_phase2_exact, domain_poly,
                      output_binade_pieces, pack_slice)
@@ -143,8 +144,8 @@ class SliceOutput:
     batch: SliceBatch
     fail_global: np.ndarray    # uint64 phase-1 failing global domain ids (ascending)
     sub_table: tuple           # uint64 arrays (parent id, sub index, start, count), ascending
-    candidates: list           # HrCaseRecord candidates of phase 3 (argument order)
-    records: list              # confirmed HR records (sorted)
+    candidates: object         # RecordSet of phase-3 candidates (argument order; a Sequence of HrCaseRecord)
+    records: object            # RecordSet of confirmed HR records (sorted)
     stats: PhaseStats
     iterations: int            # phase-1 quotient steps (SearchOutcome.iterations)
 
@@ -190,14 +191,11 @@ def execute_batch(batch: SliceBatch, cfg: PipelineConfig, algo: str, fn: str | N
     sub_start, sub_cnt = _sub_geometry(sub_n, sub_j, split)
     stats.rows.append(PhaseRow("phase2", len(res.fail_ids), len(res.sub_keys), int(fail_sizes.sum()),
                                res.phase_ms[1]))
-    cand = [HrCaseRecord(index_bits(batch.binade, int(m), fmt), UFrac(int(dd), 64), id0 + int(dm))
-            for m, dd, dm in zip(res.cand_index.tolist(), res.cand_dist.tolist(), res.cand_dom.tolist())]
+    cand = RecordSet(fmt.precision, batch.binade, res.cand_index, res.cand_dist, res.cand_dom + np.uint64(id0))
     stats.rows.append(PhaseRow("phase3", len(res.sub_keys), len(cand), int(sub_cnt.sum()), res.phase_ms[2]))
-    records = []
     t4 = time.perf_counter()
-    if confirm:
-        records = confirm_candidates(fn or cfg.fn, cand, fmt, workers if workers is not None else
-                                     cfg.phase.parallel_width)
+    records = confirm_set(fn or cfg.fn, cand, fmt, workers if workers is not None else cfg.phase.parallel_width) \
+        if confirm else RecordSet(fmt.precision, batch.binade, [], [], [])
     stats.rows.append(PhaseRow("confirm", len(cand), len(records), len(cand), (time.perf_counter() - t4) * 1e3))
     table = (sub_local + np.uint64(id0), sub_j, sub_start, sub_cnt)
     return SliceOutput(batch, res.fail_ids + np.uint64(id0), table, cand, records, stats, res.iterations)
@@ -224,14 +222,11 @@ def execute_batch_host(batch: SliceBatch, cfg: PipelineConfig, algo: str, fn: st
     stats = PhaseStats()
     stats.rows.append(PhaseRow("phase1", batch.n_total, n_fail, batch.arguments, res.device_ms))
     stats.rows.append(PhaseRow("phase2", n_fail, n_sub, a2, 0.0))
-    cand = [HrCaseRecord(index_bits(batch.binade, int(m), fmt), UFrac(int(dd), 64), id0 + int(dm))
-            for m, dd, dm in zip(res.cand_index.tolist(), res.cand_dist.tolist(), res.cand_dom.tolist())]
+    cand = RecordSet(fmt.precision, batch.binade, res.cand_index, res.cand_dist, res.cand_dom + np.uint64(id0))
     stats.rows.append(PhaseRow("phase3", n_sub, n_cand, a3, 0.0))
-    records = []
     t4 = time.perf_counter()
-    if confirm:
-        records = confirm_candidates(fn or cfg.fn, cand, fmt, workers if workers is not None else
-                                     cfg.phase.parallel_width)
+    records = confirm_set(fn or cfg.fn, cand, fmt, workers if workers is not None else cfg.phase.parallel_width) \
+        if confirm else RecordSet(fmt.precision, batch.binade, [], [], [])
     stats.rows.append(PhaseRow("confirm", len(cand), len(records), len(cand), (time.perf_counter() - t4) * 1e3))
     return SliceOutput(batch, None, None, cand, records, stats, iters)
 
@@ -276,6 +271,28 @@ def _confirm_native(fn: str, cand: list, fmt: FpFormat, workers: int):
         elif h:
             records.append(HrCaseRecord(c.argument, UFrac(int(d), 64), c.domain_id))
     return records, rest
+
+
+def confirm_set(fn: str, cand: RecordSet, fmt: FpFormat, workers: int = 1) -> RecordSet:
+    """confirm_candidates on a RecordSet of candidates, staying in arrays:
+    the native decide_hr (hostgen) runs on the index column and only the
+    candidates it hands back (and functions it does not cover) go through
+    the Python decide_hr.  Same records, sorted."""
+    from . import hostgen
+
+    p, binade = fmt.precision, cand.binade
+    if fn in hostgen.FN_CODES and binade <= 0 and len(cand):
+        cfg = hostgen.make_cfg(fn, fmt, PolyGenConfig(delta=2), binade, 64)
+        is_hr, dist, status = hostgen.confirm(cfg, cand.index, workers)
+        ok = status == hostgen.HRBH_OK
+        keep = ok & (is_hr != 0)
+        recs = RecordSet(p, binade, cand.index[keep], dist[keep], cand.dom[keep])
+        if ok.all():
+            return recs
+        rest = [cand[int(k)] for k in np.flatnonzero(~ok)]
+        more = confirm_candidates(fn, rest, fmt, workers, native=False)
+        return RecordSet.concat([recs, more], p, binade).sorted()
+    return RecordSet.of(confirm_candidates(fn, list(cand), fmt, workers), p, binade)
 
 
 def confirm_candidates(fn: str, cand: Sequence[HrCaseRecord], fmt: FpFormat, workers: int = 1,
@@ -330,7 +347,7 @@ def run_pipeline(binade: int, cfg: PipelineConfig, prev_stats: PhaseStats | None
         algo = select_algorithm(prev_stats)
     out = run_slice(cfg.fn, binade, 0, 1 << (cfg.fmt.precision - 1), cfg, algo)
     out.stats.algorithm_choices.append((binade, algo))
-    return out.records, out.stats
+    return list(out.records), out.stats
 
 
 @dataclass
@@ -338,7 +355,7 @@ class RangeOutput:
     """run_range's result: records of the whole range (ascending) and one
     PhaseStats per interval, with the algorithm each interval used."""
 
-    records: list
+    records: object   # RecordSet (a Sequence of HrCaseRecord), ascending
     interval_stats: list
     choices: list  # (first argument index, algorithm) per interval
 
@@ -432,7 +449,7 @@ def execute_wide(batch, cfg: PipelineConfig, algo: str, fn: str | None = None, c
     """A high-degree slice (wide.WideSliceBatch) through ONE host-buffer ABI
     call (hrb_wrun_slice_host), then the rigorous confirmation; statistics
     as execute_batch_host.  The wide kernels run the regular family."""
-    from .wide import candidates_of, run_wide_host
+    from .wide import run_wide_host
 
     if algo not in ("regular", "regular_unrolled"):
         raise ValueError("high-degree slices run the regular search family")
@@ -441,13 +458,13 @@ def execute_wide(batch, cfg: PipelineConfig, algo: str, fn: str | None = None, c
     stats = PhaseStats()
     stats.rows.append(PhaseRow("phase1", batch.n_total, n_fail, batch.arguments, res.device_ms))
     stats.rows.append(PhaseRow("phase2", n_fail, n_sub, a2, 0.0))
-    cand = candidates_of(batch, res)
+    cand = RecordSet(cfg.fmt.precision, batch.binade, res.cand_index, res.cand_dist,
+                     res.cand_dom + np.uint64(batch.id0))
     stats.rows.append(PhaseRow("phase3", n_sub, n_cand, a3, 0.0))
-    records = []
     t4 = time.perf_counter()
-    if confirm:
-        records = confirm_candidates(fn or cfg.fn, cand, cfg.fmt, workers if workers is not None else
-                                     cfg.phase.parallel_width)
+    records = confirm_set(fn or cfg.fn, cand, cfg.fmt, workers if workers is not None else
+                          cfg.phase.parallel_width) if confirm else RecordSet(cfg.fmt.precision, batch.binade, [],
+                                                                              [], [])
     stats.rows.append(PhaseRow("confirm", len(cand), len(records), len(cand), (time.perf_counter() - t4) * 1e3))
     return SliceOutput(batch, None, None, cand, records, stats, iters)
 
@@ -526,7 +543,7 @@ def run_range(fn: str, binade: int, start: int, count: int, cfg: PipelineConfig,
             for k, part in enumerate(parts):
                 if k in done:  # restored from the manifest
                     bstart, algo, recs, st = done[k]
-                    records.extend(recs)
+                    records.append(recs)
                     stats_list.append(st)
                     choices.append((bstart, algo))
                     prev = st
@@ -543,7 +560,7 @@ def run_range(fn: str, binade: int, start: int, count: int, cfg: PipelineConfig,
                 else:
                     out = execute_batch_host(batch, cfg, algo, fn, confirm=confirm, workers=w)
                 out.stats.algorithm_choices.append((bstart_of[k], algo))
-                records.extend(out.records)
+                records.append(out.records)
                 stats_list.append(out.stats)
                 choices.append((bstart_of[k], algo))
                 prev = out.stats
@@ -554,8 +571,7 @@ def run_range(fn: str, binade: int, start: int, count: int, cfg: PipelineConfig,
     finally:
         if sink is not None:
             sink.close()
-    records.sort()
-    return RangeOutput(records, stats_list, choices)
+    return RangeOutput(RecordSet.concat(records, cfg.fmt.precision, binade).sorted(), stats_list, choices)
 
 
 # --------------------------------------------------- per-phase drop-ins
