@@ -259,6 +259,20 @@ int hrb_wrun_slice_host(const hrb_wslice* host_slice, int algo, int split, uint6
  */
 int hrb_wdomain_coefficients(const hrb_wslice* s, uint32_t* out, void* stream);
 
+/*
+ * Rigorous confirmation of candidates on the device: decide_hr for exp
+ * (evalf.py:286-327) at the pipeline's start precision 2 (p + eps_bits) + 16
+ * (pipeline.py:446-461), for n candidates given by their binade argument
+ * index (binade <= 0).  is_hr[i]; for HR cases dist_raw[i] =
+ * floor(distance_lo 2^64) (UFrac.from_fraction of HrDecision.distance_lo);
+ * status[i] = 1 when the device did not settle the candidate (the host's
+ * hrbh_confirm / decide_hr does).  The device runs the same exact
+ * restatement of mpmath's interval exp as libhrbhost.so (csrc/host/).
+ * All pointers are device pointers.
+ */
+int hrb_confirm_exp(int precision, int eps_bits, int binade, int64_t n, const uint64_t* index, uint8_t* is_hr,
+                    uint64_t* dist_raw, uint8_t* status, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

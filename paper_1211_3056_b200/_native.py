@@ -37,6 +37,7 @@ EXPORTS = (
     "hrb_wrun_slice",
     "hrb_wrun_slice_host",
     "hrb_wdomain_coefficients",
+    "hrb_confirm_exp",
 )
 
 
@@ -124,6 +125,7 @@ def _declare(lib) -> None:
     lib.hrb_wrun_slice.argtypes = [C.POINTER(HrbWSlice), I, I, C.POINTER(HrbRunOut), P]
     lib.hrb_wrun_slice_host.argtypes = [C.POINTER(HrbWSlice), I, I, P, P, P, P, U64, C.POINTER(C.c_float)]
     lib.hrb_wdomain_coefficients.argtypes = [C.POINTER(HrbWSlice), P, P]
+    lib.hrb_confirm_exp.argtypes = [I, I, I, I64, P, P, P, P, P]
     for name in EXPORTS:
         if name not in ("hrb_version", "hrb_last_error"):
             getattr(lib, name).restype = I

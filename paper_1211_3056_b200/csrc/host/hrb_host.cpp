@@ -12,6 +12,7 @@
 
 #include "bign.h"
 #include "mpexp.h"
+#include "decide.h"
 
 using namespace hrbh;
 
@@ -238,87 +239,6 @@ int hrbh_pack_blocks(const hrbh_cfg* cfg, int64_t S_, const uint64_t* index_star
 
 namespace {
 
-// evalf._dist_range (reference evalf.py:209-232 _dist_interval)
-void dist_range(const U& off, const U& width, const U& grid, U* dlo, U* dhi) {
-    U end = add(off, width);
-    U half = shr(grid, 1);
-    if (cmp(end, grid) >= 0) {
-        *dlo = U();
-        if (cmp(off, half) <= 0) {
-            *dhi = half;
-        } else {
-            U a = sub(grid, off);
-            U eg = sub(end, grid);
-            U b = cmp(eg, half) < 0 ? eg : half;
-            *dhi = cmp(a, b) > 0 ? a : b;
-        }
-        return;
-    }
-    U go = sub(grid, off), ge = sub(grid, end);
-    U d0 = cmp(off, go) < 0 ? off : go;
-    U d1 = cmp(end, ge) < 0 ? end : ge;
-    *dlo = cmp(d0, d1) < 0 ? d0 : d1;
-    if (cmp(off, half) <= 0 && cmp(half, end) <= 0)
-        *dhi = half;
-    else
-        *dhi = cmp(d0, d1) > 0 ? d0 : d1;
-}
-
-// bit length of the reduced denominator of m 2^e (m > 0)
-int den_bits(const U& m, int e) {
-    int ee = e + m.tz();
-    return ee >= 0 ? 1 : -ee + 1;
-}
-
-// 0 = not HR, 1 = HR (dist set), -1 = fallback
-int decide_exp(const hrbh_cfg& c, uint64_t index, uint64_t* dist) {
-    overflow_flag() = false;
-    const int p = c.precision;
-    const int xe = c.binade + 1 - p;
-    const uint64_t M = (1ull << (p - 1)) + index;
-    int prec = 2 * (p + c.eps_bits) + 16;
-    while (prec <= 4096) {
-        Enc en;
-        if (!exp_enclose(M, xe, prec, &en)) return -1;
-        // lo == hi (exactly representable at this precision): rare; Python
-        if (cmp(en.lm, en.hm) == 0) return -1;
-        const int sc = std::max(std::max(den_bits(en.lm, en.le), den_bits(en.hm, en.he)), prec) + 4;
-        // nlo = floor(lo 2^sc), nhi = ceil(hi 2^sc)
-        U nlo = en.le + sc >= 0 ? shl(en.lm, en.le + sc) : shr(en.lm, -(en.le + sc));
-        U nhi;
-        if (en.he + sc >= 0) {
-            nhi = shl(en.hm, en.he + sc);
-        } else {
-            int k = -(en.he + sc);
-            nhi = shr(en.hm, k);
-            if (!en.hm.low_zero(k)) nhi = add(nhi, U(1));
-        }
-        if (nlo.bitlen() == nhi.bitlen()) {
-            const int e = nlo.bitlen() - sc;
-            const int gbits = sc + e - p;
-            if (gbits > 0) {
-                U grid = pow2(gbits);
-                U dlo, dhi;
-                dist_range(low_bits(nlo, gbits), sub(nhi, nlo), grid, &dlo, &dhi);
-                // compare against eps = 2^-eps_bits in grid units
-                auto lt_eps = [&](const U& d) {
-                    if (gbits >= c.eps_bits) return cmp(d, pow2(gbits - c.eps_bits)) < 0;
-                    return d.zero();
-                };
-                if (overflow_flag()) return -1;
-                if (lt_eps(dhi)) {
-                    U r = gbits >= 64 ? shr(dlo, gbits - 64) : shl(dlo, 64 - gbits);
-                    *dist = r.low64();
-                    return 1;
-                }
-                if (!lt_eps(dlo)) return 0;
-            }
-        }
-        prec *= 2;
-    }
-    return -1;  // undecided at the cap: the Python path raises UndecidedError
-}
-
 }  // namespace
 
 extern "C" {
@@ -331,7 +251,7 @@ int hrbh_confirm(const hrbh_cfg* cfg, int64_t n, const uint64_t* index, uint8_t*
 #pragma omp parallel for schedule(dynamic, 8) num_threads(threads)
     for (int64_t i = 0; i < n; i++) {
         uint64_t d = 0;
-        int r = decide_exp(c, index[i], &d);
+        int r = decide_exp(c.precision, c.eps_bits, c.binade, index[i], &d);
         status[i] = r < 0 ? HRBH_FALLBACK : HRBH_OK;
         is_hr[i] = r == 1;
         dist_raw[i] = d;

@@ -25,7 +25,7 @@ namespace hrbh {
 constexpr int EXP_MAX_WP = 400;
 
 // mpmath exp_basecase(x, prec) (libelefun.py:1086-1109)
-inline U exp_basecase(const U& x, int prec) {
+HRBH_HD U exp_basecase(const U& x, int prec) {
     int r = (int)isqrt_u64((uint64_t)prec);
     const int P = prec + r;
     U s0 = pow2(P), s1 = s0;
@@ -57,12 +57,12 @@ struct Enc {
     int le = 0, he = 0;
 };
 
-inline int reduced_bits(uint64_t M, int xe, int* den_bits) {
+HRBH_HD int reduced_bits(uint64_t M, int xe, int* den_bits) {
     // X = M 2^xe as a reduced fraction num / den
-    int tz = __builtin_ctzll(M);
+    int tz = ctz64(M);
     uint64_t num = M >> tz;
     int e = xe + tz;
-    int nb = 64 - __builtin_clzll(num);
+    int nb = 64 - clz64(num);
     if (e >= 0) {
         *den_bits = 1;
         return nb + e;
@@ -71,17 +71,17 @@ inline int reduced_bits(uint64_t M, int xe, int* den_bits) {
     return nb;
 }
 
-inline bool exp_enclose(uint64_t M, int xe, int prec, Enc* out) {
+HRBH_HD bool exp_enclose(uint64_t M, int xe, int prec, Enc* out) {
     if (M == 0) return false;
     int den_bits;
     int num_bits = reduced_bits(M, xe, &den_bits);
-    int work = std::max(prec, std::max(num_bits, den_bits)) + 8;
+    int work = imax(prec, imax(num_bits, den_bits)) + 8;
     int wp = work + 14;
     // mpmath's mag = bitcount(man) + exp = floor(log2 X) + 1
-    int mag = (63 - __builtin_clzll(M)) + xe + 1;
+    int mag = (63 - clz64(M)) + xe + 1;
     if (mag > 1 || mag < -wp || wp > EXP_MAX_WP) return false;
     // t = X * 2^wp; offset = exp + wp where X = man 2^exp (man odd)
-    int tz = __builtin_ctzll(M);
+    int tz = ctz64(M);
     U man((uint64_t)(M >> tz));
     int offset = xe + tz + wp;
     U t = offset >= 0 ? shl(man, offset) : shr(man, -offset);
@@ -95,7 +95,11 @@ inline bool exp_enclose(uint64_t M, int xe, int prec, Enc* out) {
     out->hm = ce;
     out->le = n - wp;
     out->he = n - wp;
+#if defined(__CUDA_ARCH__)
+    return true;  // device callers stay within the capacity (confirm.cuh)
+#else
     return !overflow_flag();
+#endif
 }
 
 }  // namespace hrbh

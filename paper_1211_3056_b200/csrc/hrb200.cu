@@ -32,6 +32,7 @@
 #include <vector>
 
 #include "../../include/hrb200.h"
+#include "confirm.cuh"
 #include "search_core.cuh"
 #include "tile_search.cuh"
 
@@ -2262,3 +2263,42 @@ int hrb_wrun_slice_host(const hrb_wslice* hs, int algo, int split, uint64_t* cou
 }
 
 }  // extern "C"
+
+// ===========================================================================
+// rigorous confirmation on the device: csrc/confirm.cuh
+// ===========================================================================
+extern "C" int hrb_confirm_exp(int precision, int eps_bits, int binade, int64_t n, const uint64_t* index,
+                               uint8_t* is_hr, uint64_t* dist_raw, uint8_t* status, void* stream) {
+    if (precision < 2 || precision > 64 || eps_bits < 1 || binade > 0 || binade < -1000 || n < 0)
+        return set_err(HRB_ERR_CONFIG, "hrb_confirm_exp: exp on binades <= 0, 2 <= p <= 64, eps_bits >= 1");
+    if (n == 0) return HRB_OK;
+    static std::atomic<bool> inv_ready{false};
+    if (!inv_ready.load()) {  // ceil(2^64 / d) for the fast kernel's small divisions
+        uint64_t inv[128] = {0, 0};
+        for (int d = 2; d < 128; d++) inv[d] = (uint64_t)(((unsigned __int128)1 << 64) / d) + 1;
+        CK(cudaMemcpyToSymbol(fw::c_inv, inv, sizeof(inv)));
+        inv_ready = true;
+    }
+    int grid = (int)((n + 127) / 128);
+    if (grid > sm_count() * 16) grid = sm_count() * 16;
+    // the first precision step's widest value has P + 3 bits (see confirm.cuh)
+    const int prec0 = 2 * (precision + eps_bits) + 16;
+    int work = prec0 > 64 ? prec0 : 64;
+    if (precision - binade + 1 > work) work = precision - binade + 1;
+    work += 8;
+    const int wp = work + 14;
+    int r = 0;
+    while ((r + 1) * (r + 1) <= wp) r++;
+    const int nl = (wp + r + 3 + 63) / 64;
+    cudaStream_t st = (cudaStream_t)stream;
+#define FAST(NLV) confirm_exp_fast_kernel<NLV><<<grid, 128, 0, st>>>(precision, eps_bits, binade, prec0, n, index, \
+                                                                       is_hr, dist_raw, status)
+    if (nl <= 3) FAST(3);
+    else if (nl == 4) FAST(4);
+    else if (nl == 5) FAST(5);
+    else if (nl == 6) FAST(6);
+    else confirm_exp_kernel<<<grid, 128, 0, st>>>(precision, eps_bits, binade, n, index, is_hr, dist_raw, status);
+#undef FAST
+    CK(cudaGetLastError());
+    return HRB_OK;
+}

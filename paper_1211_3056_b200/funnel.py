@@ -273,6 +273,38 @@ def _confirm_native(fn: str, cand: list, fmt: FpFormat, workers: int):
     return records, rest
 
 
+DEVICE_CONFIRM_MIN = 4096  # candidates from which the device confirmation pays for its copies
+
+
+def _cuda_ready() -> bool:
+    try:
+        import torch
+
+        return torch.cuda.is_available()
+    except Exception:  # pragma: no cover
+        return False
+
+
+def confirm_on_device(fmt: FpFormat, binade: int, index: np.ndarray):
+    """hrb_confirm_exp over host arrays: (is_hr, dist_raw, status), the
+    device running the same exact decide_hr restatement as the host
+    library (csrc/host/decide.h)."""
+    import ctypes as C
+
+    torch = nat.require_cuda()
+    lib = nat.load()
+    n = len(index)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    idx = torch.from_numpy(np.ascontiguousarray(index, dtype=np.uint64).view(np.int64)).to(dev)
+    is_hr = torch.empty(n, dtype=torch.uint8, device=dev)
+    st = torch.empty(n, dtype=torch.uint8, device=dev)
+    dist = torch.empty(n, dtype=torch.int64, device=dev)
+    nat.check("hrb_confirm_exp", lib.hrb_confirm_exp(fmt.precision, fmt.eps_bits, binade, n, idx.data_ptr(),
+                                                     is_hr.data_ptr(), dist.data_ptr(), st.data_ptr(),
+                                                     nat.stream_ptr()))
+    return (is_hr.cpu().numpy(), dist.cpu().numpy().view(np.uint64).copy(), st.cpu().numpy())
+
+
 def confirm_set(fn: str, cand: RecordSet, fmt: FpFormat, workers: int = 1) -> RecordSet:
     """confirm_candidates on a RecordSet of candidates, staying in arrays:
     the native decide_hr (hostgen) runs on the index column and only the
@@ -282,8 +314,16 @@ def confirm_set(fn: str, cand: RecordSet, fmt: FpFormat, workers: int = 1) -> Re
 
     p, binade = fmt.precision, cand.binade
     if fn in hostgen.FN_CODES and binade <= 0 and len(cand):
-        cfg = hostgen.make_cfg(fn, fmt, PolyGenConfig(delta=2), binade, 64)
-        is_hr, dist, status = hostgen.confirm(cfg, cand.index, workers)
+        if len(cand) >= DEVICE_CONFIRM_MIN and _cuda_ready():
+            is_hr, dist, status = confirm_on_device(fmt, binade, cand.index)
+            if status.any():  # whatever the device left goes to the host library
+                rest = np.flatnonzero(status != 0)
+                cfg = hostgen.make_cfg(fn, fmt, PolyGenConfig(delta=2), binade, 64)
+                h_is, h_d, h_st = hostgen.confirm(cfg, cand.index[rest], workers)
+                is_hr[rest], dist[rest], status[rest] = h_is, h_d, h_st
+        else:
+            cfg = hostgen.make_cfg(fn, fmt, PolyGenConfig(delta=2), binade, 64)
+            is_hr, dist, status = hostgen.confirm(cfg, cand.index, workers)
         ok = status == hostgen.HRBH_OK
         keep = ok & (is_hr != 0)
         recs = RecordSet(p, binade, cand.index[keep], dist[keep], cand.dom[keep])
@@ -291,7 +331,7 @@ def confirm_set(fn: str, cand: RecordSet, fmt: FpFormat, workers: int = 1) -> Re
             return recs
         rest = [cand[int(k)] for k in np.flatnonzero(~ok)]
         more = confirm_candidates(fn, rest, fmt, workers, native=False)
-        return RecordSet.concat([recs, more], p, binade).sorted()
+        return recs.merged(RecordSet.of(more, p, binade))
     return RecordSet.of(confirm_candidates(fn, list(cand), fmt, workers), p, binade)
 
 

@@ -127,3 +127,35 @@ def test_measure_warps_matches_oracle_iterations():
         want = [float(nmdm(it[w * 32:(w + 1) * 32].tolist())) for w in range(n // 32)]
         assert np.allclose(s.warp_nmdm, want, rtol=0, atol=1e-12)
         assert len(s.warp_max) == n // 32
+
+
+@pytest.mark.parametrize("p,eps_bits,binade", [(53, 16, 0), (53, 32, 0), (53, 20, -1), (24, 12, 0), (13, 6, -2)])
+def test_device_confirmation_equals_host_and_decide_hr(p, eps_bits, binade):
+    """hrb_confirm_exp (the device running csrc/host/decide.h) gives the
+    host library's decisions and distances, which equal decide_hr's; plus
+    arguments near HR (from the reference's own candidates) at p = 53."""
+    from paper_1211_3056_b200 import hostgen
+    from paper_1211_3056_b200.enclosure import decide_hr
+    from paper_1211_3056_b200.fpformat import FpFormat, bits_float
+    from paper_1211_3056_b200.arith import UFrac
+    from paper_1211_3056_b200.funnel import confirm_on_device
+    from paper_1211_3056_b200.taylor import PolyGenConfig
+
+    fmt = FpFormat(p, eps_bits)
+    rng = np.random.default_rng(p * 100 + eps_bits)
+    idx = rng.integers(0, 1 << (p - 1), 20000, dtype=np.uint64)
+    if p == 53 and binade == 0:
+        c = case("p53_exp_2p20_e16_N15")
+        idx = np.concatenate([idx, np.array([int(a, 16) & ((1 << 52) - 1) for a, _, _ in c["phase3"]],
+                                            dtype=np.uint64)])
+    d_is, d_dist, d_st = confirm_on_device(fmt, binade, idx)
+    assert (d_st == 0).all()
+    cfg = hostgen.make_cfg("exp", fmt, PolyGenConfig(), binade, 64)
+    h_is, h_dist, h_st = hostgen.confirm(cfg, idx, 4)
+    assert np.array_equal(d_is, h_is) and np.array_equal(d_dist[d_is == 1], h_dist[h_is == 1])
+    for k in list(np.flatnonzero(d_is))[:40] + list(range(0, len(idx), 997)):
+        arg = ((binade + 1 + (1 << 15)) << (p - 1)) | int(idx[k])
+        dec = decide_hr("exp", bits_float(arg, fmt), fmt, start_prec=2 * (p + eps_bits) + 16)
+        assert bool(d_is[k]) == dec.is_hr
+        if dec.is_hr:
+            assert int(d_dist[k]) == UFrac.from_fraction(dec.distance_lo).raw
