@@ -780,31 +780,55 @@ __global__ void __launch_bounds__(256, HRB_P3_MINB) phase3_kernel(SliceDev s, in
                 mbase = __ldg(&s.m0[t]) + i * (uint64_t)__ldg(&s.dom_n[t]) + o;
             }
         }
-        const uint64_t Khi = (uint64_t)(K >> 64);
+        // Hot loop on a 32-bit proxy of the top word: u = top32(V) + MARGIN,
+        // stepped by the top words of D1 and D2.  Floors of sums exceed sums
+        // of floors by at most one per term, so after x < 32 steps the true
+        // top word T(x) lies in [u - MARGIN, u - MARGIN + x + C(x,2)] (<= 496):
+        // V < K  =>  T <= top32(K)  =>  u <= top32(K) + MARGIN (no wrap on
+        // either side).  Two instructions per argument; the exact 128-bit
+        // state advances once per 32 arguments and a block is re-examined
+        // only when some lane's proxy flagged it.
+        constexpr uint32_t MARGIN = 1024;
         const uint32_t Ktop = (uint32_t)(K >> 96);
+        const uint32_t KtopM = Ktop > 0xFFFFFFFFu - MARGIN ? 0xFFFFFFFFu : Ktop + MARGIN;
+        const uint32_t e32 = (uint32_t)(D2 >> 96), e2x32 = 2 * e32;
+        const u128 D2x32 = D2 << 5, D2x496 = D2 * (u128)496;
         uint32_t rank = 0;
-        R96 v96 = r96_of(V), d96 = r96_of(D1), e96 = r96_of(D2);
         for (uint32_t x0 = 0; x0 < CHUNK3; x0 += 32) {
-            const u128 V0 = NARROW ? u128_of(v96) : V, D10 = NARROW ? u128_of(d96) : D1;
-            bool any = false;
-            uint32_t lo_top = 0xFFFFFFFFu;  // min of the top words over the 32 arguments (one VIMNMX each)
-#pragma unroll 16
-            for (uint32_t x = 0; x < 32; x++) {
-                if (NARROW) {
-                    lo_top = min(lo_top, v96.h1);  // conservative: V < K implies top32(V) <= top32(K)
-                    add96_alu(v96, d96);
-                    add96_fma(d96, e96);
-                } else {
-                    any |= (uint64_t)(V >> 64) <= Khi;
-                    V += D1;
-                    D1 += D2;
-                }
+            const u128 V0 = V, D10 = D1;
+            uint32_t u = (uint32_t)(V >> 96) + MARGIN, d = (uint32_t)(D1 >> 96);
+            uint32_t lo_top = 0xFFFFFFFFu;
+            // two arguments per iteration, four instructions: t = u(x+1);
+            // a three-input min; u(x+2) = t + d + e as one three-input add
+            // (IADD3 -- an ALU-pipe op; two-input adds alone all went to the
+            // FMA pipe as IMAD.IADD and throttled it); d(x+2) = d + 2e
+#pragma unroll
+            for (uint32_t x = 0; x < 32; x += 2) {
+                const uint32_t t = u + d;
+                lo_top = min(lo_top, min(u, t));
+                u = t + d + e32;
+                d += e2x32;
             }
-            if (NARROW) any = lo_top <= Ktop;
-            if (__any_sync(0xffffffffu, any)) {  // rare: re-walk exactly and append in order
-                u128 v = V0, d = D10;
+            V += (D1 << 5) + D2x496;  // exact: 32 steps of V += D1, D1 += D2
+            D1 += D2x32;
+            const bool any = x0 < len && lo_top <= KtopM;
+            if (__any_sync(0xffffffffu, any)) {
+                // rare: replay the proxy over the block; only the arguments it
+                // flags (the true hits, and near-misses within MARGIN of the
+                // window's top word) are evaluated exactly -- V(x) = V0 +
+                // x D1 + C(x,2) D2 -- and appended in argument order
+                uint32_t pu = (uint32_t)(V0 >> 96) + MARGIN, pd = (uint32_t)(D10 >> 96);
                 for (uint32_t x = 0; x < 32; x++) {
-                    const bool hit = (x0 + x < len) && v < K;
+                    const bool flag = any && x0 + x < len && pu <= KtopM;
+                    pu += pd;
+                    pd += e32;
+                    if (!__any_sync(0xffffffffu, flag)) continue;
+                    bool hit = false;
+                    u128 v = 0;
+                    if (flag) {
+                        v = V0 + D10 * (u128)x + D2 * (u128)((x * (x - 1)) >> 1);
+                        hit = v < K;
+                    }
                     const uint32_t ball = __ballot_sync(0xffffffffu, hit);
                     if (ball) {
                         const int leader = __ffs(ball) - 1;
@@ -827,8 +851,6 @@ __global__ void __launch_bounds__(256, HRB_P3_MINB) phase3_kernel(SliceDev s, in
                             rank++;
                         }
                     }
-                    v += d;
-                    d += D2;
                 }
             }
         }

@@ -19,6 +19,7 @@ def main():
     ap.add_argument("--start", type=lambda x: int(x, 0), default=0)
     ap.add_argument("--launches", type=int, default=1)
     ap.add_argument("--no-peak", action="store_true")
+    ap.add_argument("--cand-cap", type=int, default=1 << 20)
     a = ap.parse_args()
     ns = argparse.Namespace(log2_args=a.log2_args, eps_bits=a.eps_bits, algo=a.algo, log2_super=24, log2_N=15,
                             fn=a.fn, start=a.start)
@@ -28,7 +29,7 @@ def main():
 
     batch, _ = bench.prepare_rank(ns, 0, 1, os.cpu_count() or 1)
     ds = DeviceSlice(batch)
-    r = FusedRunner(ds, 2 if a.algo == "regular" else 0, 1, 8, sub_cap=batch.n_total * 2, cand_cap=1 << 20)
+    r = FusedRunner(ds, 2 if a.algo == "regular" else 0, 1, 8, sub_cap=batch.n_total * 2, cand_cap=a.cand_cap)
     for _ in range(a.launches):
         r.launch()
     torch.cuda.synchronize()
