@@ -204,7 +204,15 @@ __global__ void __launch_bounds__(64) wseed_kernel(WideDev w, const uint64_t* ti
         __syncthreads();  // the previous tile's binomials are consumed
         if (c <= w.D) {
             uint32_t b[NL];
-            binom_big<NL>(i0, c, b);
+            if (i0 < (1ull << 25) && c <= 5) {  // C(i0, c) < 2^125: exact in 128 bits, no divisions
+                u128 bb[6];
+                binoms_u128<5>(i0, bb);
+                const u128 v = bb[c];
+#pragma unroll
+                for (int q = 0; q < NL; q++) b[q] = q < 4 ? (uint32_t)(v >> (32 * q)) : 0u;
+            } else {
+                binom_big<NL>(i0, c, b);
+            }
 #pragma unroll
             for (int q = 0; q < NL; q++) bn[c][q] = b[q];
         }
