@@ -35,6 +35,7 @@
 #include "confirm.cuh"
 #include "search_core.cuh"
 #include "tile_search.cuh"
+#include "classic_lockstep.cuh"
 
 using u128 = unsigned __int128;
 
@@ -443,11 +444,11 @@ struct WalkSrc {
 // repairs; a static grid-stride split left ~17 % of the warp slots idle at
 // the end of the kernel.  The bitmap and tile_t are indexed by tile, so the
 // output does not depend on which warp ran which tile.
-template <int W, int SH, int PL>
+template <int W, int SH, int PL, bool CL = false>
 __global__ void __launch_bounds__(128, HRB_P1_MINB) phase1_reg_kernel(SliceDev s, int algo, const uint64_t* tile_base,
                                                           uint32_t* bitmap, uint32_t* tile_t,
                                                           unsigned long long* iter_sum,
-                                                          unsigned long long* tile_ctr) {
+                                                          unsigned long long* tile_ctr, int mode = 1) {
     __shared__ Walk walks[128];
     __shared__ u128 incs[4][2];
     const int lane = threadIdx.x & 31;
@@ -493,7 +494,9 @@ __global__ void __launch_bounds__(128, HRB_P1_MINB) phase1_reg_kernel(SliceDev s
         }
         __syncwarp();
         unsigned long long its = 0;
-        const uint32_t fails = hrb::lane_items<W, NU>(src, &its, algo == hrb::ALGO_REGULAR_UNROLLED, nper);
+        // CL: the classic family (classic_lockstep.cuh), else the regular one
+        const uint32_t fails = CL ? hrb::lane_items_classic<W, NU>(src, &its, mode, nper)
+                                  : hrb::lane_items<W, NU>(src, &its, algo == hrb::ALGO_REGULAR_UNROLLED, nper);
         iters += its;
         uint32_t mine = 0;
 #pragma unroll
@@ -542,11 +545,11 @@ struct SubWalkSrc {
     __device__ __forceinline__ void done(int, bool, uint64_t, uint32_t) {}
 };
 
-template <int W, int SH>
+template <int W, int SH, bool CL = false>
 __global__ void __launch_bounds__(128, HRB_P2_MINB) phase2_reg_kernel(SliceDev s, int split, const uint64_t* fail_ids,
                                                           const uint32_t* fail_t, const uint64_t* fail_count,
                                                           uint64_t fail_cap, unsigned long long* meta,
-                                                          uint32_t* bitmap) {
+                                                          uint32_t* bitmap, int mode = 1) {
     uint64_t nf = *fail_count;
     if (nf > fail_cap) nf = fail_cap;
     const uint32_t J = (uint32_t)meta[0];
@@ -596,7 +599,9 @@ __global__ void __launch_bounds__(128, HRB_P2_MINB) phase2_reg_kernel(SliceDev s
         for (uint32_t c = 0; c < wpd; c++) {
             src.base = 32 * c;
             unsigned long long its = 0;
-            const uint32_t fails = hrb::lane_items<W, 32>(src, &its, false, src.nsub > 32 * c ? src.nsub - 32 * c : 0);
+            const uint32_t nit = src.nsub > 32 * c ? src.nsub - 32 * c : 0;
+            const uint32_t fails = CL ? hrb::lane_items_classic<W, 32>(src, &its, mode, nit)
+                                      : hrb::lane_items<W, 32>(src, &its, false, nit);
             if (valid) bitmap[f * wpd + c] = fails;
         }
         chunk = __shfl_sync(0xffffffffu, next, 0);
@@ -1567,9 +1572,20 @@ int phase1_impl(Workspace& ws, const hrb_slice* s, const SliceDev& sd0, int algo
             if (quarter) P1(32, -1, 2); else P1(32, -1, 0);
         }
 #undef P1
-    } else {
-        if (sd.W == 64) phase1_kernel<64, false><<<grid, 256, 0, st>>>(sd, algo, mode, tb, bm, tt, is);
-        else phase1_kernel<32, false><<<grid, 256, 0, st>>>(sd, algo, mode, tb, bm, tt, is);
+    } else {  // the classic family: lockstep pairs with refill (classic_lockstep.cuh)
+        const int g5 = sm_count() * HRB_P1_MINB;
+        const bool quarter = (uint64_t)s->n_total / TILE + 1 < (uint64_t)g5 * 4 * 8;
+#define P1C(WV, SHV, PLV) \
+    phase1_reg_kernel<WV, SHV, PLV, true><<<g5, 128, 0, st>>>(sd, algo, tb, bm, tt, is, tc, mode)
+        if (sd.W == 64 && sd.F == 96) {
+            if (quarter) P1C(64, 32, 2); else P1C(64, 32, 0);
+        } else if (sd.W == 64) {
+            if (quarter) P1C(64, -1, 2); else P1C(64, -1, 0);
+        } else {
+            if (quarter) P1C(32, -1, 2); else P1C(32, -1, 0);
+        }
+#undef P1C
+        (void)grid;
     }
     CK(cudaGetLastError());
     if (up.ev_data && algo >= hrb::ALGO_REGULAR && up.ready) CK(cudaStreamWaitEvent(st, up.ev_data, 0));
@@ -1602,11 +1618,18 @@ int phase2_impl(Workspace& ws, const hrb_slice* s, const SliceDev& sd, int algo,
             phase2_reg_kernel<64, -1><<<g4, 128, 0, st>>>(sd, split, fail_ids, fail_t, fail_count, fail_cap, mt, bm);
         else
             phase2_reg_kernel<32, -1><<<g4, 128, 0, st>>>(sd, split, fail_ids, fail_t, fail_count, fail_cap, mt, bm);
-    } else {
-        if (sd.W == 64)
-            phase2_classic_kernel<64><<<grid, 256, 0, st>>>(sd, mode, split, fail_ids, fail_t, fail_count, fail_cap, mt, bm);
+    } else {  // the classic family in lockstep form
+        const int g4 = sm_count() * HRB_P2_MINB;
+        if (sd.W == 64 && sd.F == 96)
+            phase2_reg_kernel<64, 32, true><<<g4, 128, 0, st>>>(sd, split, fail_ids, fail_t, fail_count, fail_cap, mt,
+                                                                bm, mode);
+        else if (sd.W == 64)
+            phase2_reg_kernel<64, -1, true><<<g4, 128, 0, st>>>(sd, split, fail_ids, fail_t, fail_count, fail_cap, mt,
+                                                                bm, mode);
         else
-            phase2_classic_kernel<32><<<grid, 256, 0, st>>>(sd, mode, split, fail_ids, fail_t, fail_count, fail_cap, mt, bm);
+            phase2_reg_kernel<32, -1, true><<<g4, 128, 0, st>>>(sd, split, fail_ids, fail_t, fail_count, fail_cap, mt,
+                                                                bm, mode);
+        (void)grid;
     }
     CK(cudaGetLastError());
     P2Compact fn{(const uint32_t*)ws.bm2.p, fail_ids, fail_t, fail_count, fail_cap, mt, sub_keys,
