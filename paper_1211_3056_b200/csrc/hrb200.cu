@@ -212,18 +212,6 @@ struct Problem {
     uint64_t a, b, eps;
 };
 
-// _boolean_problem (pipeline.py:149-175) from residues of s0, s1
-__device__ __forceinline__ Problem make_problem(u128 s0, u128 s1, uint64_t pad, int F, int W, u128 mF) {
-    Problem p;
-    u128 s0m = s0 & mF;
-    u128 s1m = (0 - s1) & mF;
-    uint64_t wmask = W == 64 ? ~0ull : ((1ull << W) - 1);
-    p.a = (uint64_t)(s1m >> (F - W));
-    p.b = ((uint64_t)(s0m >> (F - W)) + pad) & wmask;
-    p.eps = 2 * pad;
-    return p;
-}
-
 // largest t with base[t] <= x, base ascending of length S+1
 __device__ __forceinline__ int64_t find_seg(const uint64_t* base, int64_t S, uint64_t x) {
     int64_t lo = 0, hi = S - 1;
@@ -251,18 +239,6 @@ __device__ __forceinline__ uint64_t domain_size(const SliceDev& s, int64_t t, ui
 }
 
 __device__ __forceinline__ uint64_t binom2(uint64_t i) { return i ? (i * (i - 1)) >> 1 : 0; }
-
-// run one search to completion; REG selects the family at compile time so a
-// kernel instantiation carries only one loop body (register pressure)
-template <int W, bool REG>
-__device__ __forceinline__ hrb::Outcome search_one(int algo, int mode, const Problem& p, uint64_t n) {
-    if (REG) {
-        hrb::Outcome o = hrb::regular_search<W>(p.a, p.b, p.eps, n);
-        if (algo == hrb::ALGO_REGULAR_UNROLLED) o.it = (o.it + 1) >> 1;
-        return o;
-    }
-    return hrb::lefevre_search<W>(p.a, p.b, p.eps, n, mode);
-}
 
 // ---------------------------------------------------------------------------
 // prep: tiles per super-domain, max subdomain count J, max subdomain step
@@ -299,68 +275,9 @@ __global__ void prep_kernel(SliceDev s, int split, uint64_t* tiles, unsigned lon
 }
 
 // ---------------------------------------------------------------------------
-// phase 1: fused tabulated walk + Boolean test, verdict bitmap
-// ---------------------------------------------------------------------------
-template <int W, bool REG>
-__global__ void __launch_bounds__(256) phase1_kernel(SliceDev s, int algo, int mode, const uint64_t* tile_base,
-                                                     uint32_t* bitmap, uint32_t* tile_t,
-                                                     unsigned long long* iter_sum) {
-    const int lane = threadIdx.x & 31;
-    const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    const uint64_t total_tiles = tile_base[s.S];
-    const u128 mF = mask_f(s.F);
-    unsigned long long iters = 0;
-    for (uint64_t gw = warp0; gw < total_tiles; gw += nwarps) {
-        const int64_t t = locate_super(tile_base, s.S, gw);
-        const uint64_t tile = gw - tile_base[t];
-        const uint32_t nd = __ldg(&s.n_dom[t]);
-        const u128 c00 = coef_res(s, t, 0), c01 = coef_res(s, t, 1), c02 = coef_res(s, t, 2);
-        const u128 c10 = coef_res(s, t, 3), c11 = coef_res(s, t, 4);
-        const u128 G = ld128(s.G, s.S, t);
-        const u128 s2a = s.delta >= 2 ? ld128(s.s2abs, s.S, t) : (u128)0;
-        const uint64_t nfull = __ldg(&s.dom_n[t]), nlast = __ldg(&s.last_n[t]);
-        const uint64_t pad_full = pad_of(G, s2a, nfull, s.F, W);
-        const uint64_t pad_last = pad_of(G, s2a, nlast, s.F, W);
-        // seeds of the stride-32 difference tables at this lane's first domain
-        const uint64_t il = tile * TILE + lane;
-        u128 g0 = c00 + c01 * (u128)il + c02 * (u128)binom2(il);  // r0(il)
-        u128 g1 = (c01 << 5) + c02 * (u128)(32 * il + 496);       // r0(il+32) - r0(il)
-        const u128 g2 = c02 << 10;                                // second difference
-        u128 h0 = c10 + c11 * (u128)il;                           // r1(il)
-        const u128 h1 = c11 << 5;
-        uint32_t fails = 0;
-#pragma unroll 1
-        for (int k = 0; k < NU; k++) {
-            const uint64_t i = il + 32 * (uint64_t)k;
-            if (i < nd) {
-                const bool last = i == (uint64_t)nd - 1;
-                const uint64_t n = last ? nlast : nfull;
-                Problem p = make_problem(g0, h0, last ? pad_last : pad_full, s.F, W, mF);
-                hrb::Outcome o = search_one<W, REG>(algo, mode, p, n);
-                iters += o.it;
-                if (!o.ok) fails |= 1u << k;
-            }
-            g0 += g1;  // tabulated step: 3 multi-word additions per domain
-            g1 += g2;
-            h0 += h1;
-        }
-        uint32_t mine = 0;
-#pragma unroll
-        for (int k = 0; k < NU; k++) {
-            uint32_t w = __ballot_sync(0xffffffffu, (fails >> k) & 1u);
-            if (lane == k) mine = w;
-        }
-        if (lane < NU) bitmap[gw * NU + lane] = mine;
-        if (lane == 0) tile_t[gw] = (uint32_t)t;
-    }
-    // warp-reduce the iteration count, one atomic per warp
-    for (int o = 16; o > 0; o >>= 1) iters += __shfl_xor_sync(0xffffffffu, iters, o);
-    if (iter_sum && lane == 0 && iters) atomicAdd(iter_sum, iters);
-}
-
-// ---------------------------------------------------------------------------
-// regular family, throughput form (tile_search.cuh): phase 1 and phase 2
+// phases 1 and 2: fused tabulated walk + Boolean test, verdict bitmaps (the
+// regular family in tile_search.cuh's throughput form, the classic family
+// in classic_lockstep.cuh's)
 // ---------------------------------------------------------------------------
 struct Walk {  // per-lane stride-32 difference tables, in shared memory
     u128 g0, g1, h0;
@@ -444,13 +361,15 @@ struct WalkSrc {
 // repairs; a static grid-stride split left ~17 % of the warp slots idle at
 // the end of the kernel.  The bitmap and tile_t are indexed by tile, so the
 // output does not depend on which warp ran which tile.
-template <int W, int SH, int PL, bool CL = false>
+// CL: 0 the regular family, 1 + mode the classic family (classic_lockstep.cuh)
+template <int W, int SH, int PL, int CL = 0>
 __global__ void __launch_bounds__(128, HRB_P1_MINB) phase1_reg_kernel(SliceDev s, int algo, const uint64_t* tile_base,
                                                           uint32_t* bitmap, uint32_t* tile_t,
                                                           unsigned long long* iter_sum,
-                                                          unsigned long long* tile_ctr, int mode = 1) {
+                                                          unsigned long long* tile_ctr) {
     __shared__ Walk walks[128];
     __shared__ u128 incs[4][2];
+    __shared__ hrb::ClQueue clq[CL ? 4 : 1];  // the classic family's per-warp queues
     const int lane = threadIdx.x & 31;
     const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -494,9 +413,11 @@ __global__ void __launch_bounds__(128, HRB_P1_MINB) phase1_reg_kernel(SliceDev s
         }
         __syncwarp();
         unsigned long long its = 0;
-        // CL: the classic family (classic_lockstep.cuh), else the regular one
-        const uint32_t fails = CL ? hrb::lane_items_classic<W, NU>(src, &its, mode, nper)
-                                  : hrb::lane_items<W, NU>(src, &its, algo == hrb::ALGO_REGULAR_UNROLLED, nper);
+        uint32_t fails;
+        if constexpr (CL != 0)
+            fails = hrb::lane_items_classic_m<W, NU, CL - 1>(src, &clq[threadIdx.x >> 5], &its, nper);
+        else
+            fails = hrb::lane_items<W, NU>(src, &its, algo == hrb::ALGO_REGULAR_UNROLLED, nper);
         iters += its;
         uint32_t mine = 0;
 #pragma unroll
@@ -545,11 +466,12 @@ struct SubWalkSrc {
     __device__ __forceinline__ void done(int, bool, uint64_t, uint32_t) {}
 };
 
-template <int W, int SH, bool CL = false>
+template <int W, int SH, int CL = 0>  // CL as in phase1_reg_kernel
 __global__ void __launch_bounds__(128, HRB_P2_MINB) phase2_reg_kernel(SliceDev s, int split, const uint64_t* fail_ids,
                                                           const uint32_t* fail_t, const uint64_t* fail_count,
                                                           uint64_t fail_cap, unsigned long long* meta,
-                                                          uint32_t* bitmap, int mode = 1) {
+                                                          uint32_t* bitmap) {
+    __shared__ hrb::ClQueue clq[CL ? 4 : 1];  // the classic family's per-warp queues
     uint64_t nf = *fail_count;
     if (nf > fail_cap) nf = fail_cap;
     const uint32_t J = (uint32_t)meta[0];
@@ -600,61 +522,14 @@ __global__ void __launch_bounds__(128, HRB_P2_MINB) phase2_reg_kernel(SliceDev s
             src.base = 32 * c;
             unsigned long long its = 0;
             const uint32_t nit = src.nsub > 32 * c ? src.nsub - 32 * c : 0;
-            const uint32_t fails = CL ? hrb::lane_items_classic<W, 32>(src, &its, mode, nit)
-                                      : hrb::lane_items<W, 32>(src, &its, false, nit);
+            uint32_t fails;
+            if constexpr (CL != 0)
+                fails = hrb::lane_items_classic_m<W, 32, CL - 1>(src, &clq[threadIdx.x >> 5], &its, nit);
+            else
+                fails = hrb::lane_items<W, 32>(src, &its, false, nit);
             if (valid) bitmap[f * wpd + c] = fails;
         }
         chunk = __shfl_sync(0xffffffffu, next, 0);
-    }
-}
-
-// Phase 2 for the classic family: one failing domain per thread, its
-// subdomains searched one after another (the classic walk's heavy-tailed
-// iteration counts gain nothing from lockstep pairing).
-template <int W>
-__global__ void __launch_bounds__(256) phase2_classic_kernel(SliceDev s, int mode, int split, const uint64_t* fail_ids,
-                                                             const uint32_t* fail_t, const uint64_t* fail_count,
-                                                             uint64_t fail_cap, const unsigned long long* meta,
-                                                             uint32_t* bitmap) {
-    uint64_t nf = *fail_count;
-    if (nf > fail_cap) nf = fail_cap;
-    const uint32_t wpd = ((uint32_t)meta[0] + 31) >> 5;
-    for (uint64_t f = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; f < nf; f += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t id = fail_ids[f];
-        const int64_t t = fail_t[f];
-        const uint64_t i = id - __ldg(&s.dom_base[t]);
-        const uint64_t n = domain_size(s, t, i);
-        uint64_t step = udiv_small(n, (uint32_t)split);
-        if (step < 1) step = 1;
-        const uint64_t nsub = udiv_small(n + step - 1, (uint32_t)step);
-        const u128 c00 = coef_res(s, t, 0), c01 = coef_res(s, t, 1), c02 = coef_res(s, t, 2);
-        const u128 c10 = coef_res(s, t, 3), c11 = coef_res(s, t, 4);
-        const u128 s2 = s.delta >= 2 ? coef_res(s, t, 5) : (u128)0;
-        const u128 G = ld128(s.G, s.S, t);
-        const u128 s2a = s.delta >= 2 ? ld128(s.s2abs, s.S, t) : (u128)0;
-        SubWalkSrc<W> src;
-        src.sh = 128 - s.F;
-        src.t0 = c00 + c01 * (u128)i + c02 * (u128)binom2(i);
-        src.t1 = c10 + c11 * (u128)i;
-        src.dt0 = src.t1 * (u128)step + s2 * (u128)binom2(step);
-        src.d2 = s2 * (u128)(step * step);
-        src.dt1 = s2 * (u128)step;
-        src.nsub = (uint32_t)nsub;
-        src.step = (uint32_t)step;
-        src.last_cnt = (uint32_t)(n - (nsub - 1) * step);
-        src.pad_full = pad_of(G, s2a, step, s.F, W);
-        src.pad_last = pad_of(G, s2a, src.last_cnt, s.F, W);
-        for (uint32_t c = 0; c < wpd; c++) {
-            src.base = 32 * c;
-            uint32_t fails = 0;
-            for (int k = 0; k < 32; k++) {
-                uint64_t a, b, eps;
-                uint32_t N;
-                if (!src.build(k, a, b, eps, N)) break;
-                if (!hrb::lefevre_search<W>(a, b, eps, N, mode).ok) fails |= 1u << k;
-            }
-            bitmap[f * wpd + c] = fails;
-        }
     }
 }
 
@@ -675,40 +550,6 @@ struct Cand {
     uint64_t m, dist, dom, item;
     uint32_t rank;
 };
-
-// 96-bit lane registers for the phase-3 walk: value = (h1 << 96) + (h0 << 64)
-// + (m << 32), the low 32 bits being the (zero) bits below the 2^-F grid once
-// shifted by sh = 128 - F >= 32.  Three separate 32-bit words, so no 64-bit
-// packing instructions appear in the walk.  V += D1 is one ALU add chain
-// (IADD3 + 2 IADD3.X); D1 += D2 is issued as IMAD-with-carry so it runs on
-// the FMA pipe and the two chains overlap.
-struct R96 {
-    uint32_t m, h0, h1;
-};
-
-__device__ __forceinline__ R96 r96_of(u128 x) {
-    R96 r;
-    r.m = (uint32_t)(x >> 32);
-    r.h0 = (uint32_t)(x >> 64);
-    r.h1 = (uint32_t)(x >> 96);
-    return r;
-}
-
-__device__ __forceinline__ u128 u128_of(R96 r) {
-    return ((u128)r.h1 << 96) | ((u128)r.h0 << 64) | ((u128)r.m << 32);
-}
-
-__device__ __forceinline__ void add96_alu(R96& x, const R96& y) {
-    asm("add.cc.u32 %0, %0, %3;\n\taddc.cc.u32 %1, %1, %4;\n\taddc.u32 %2, %2, %5;"
-        : "+r"(x.m), "+r"(x.h0), "+r"(x.h1)
-        : "r"(y.m), "r"(y.h0), "r"(y.h1));
-}
-
-__device__ __forceinline__ void add96_fma(R96& x, const R96& y) {
-    asm("mad.lo.cc.u32 %0, %3, 1, %0;\n\tmadc.lo.cc.u32 %1, %4, 1, %1;\n\tmadc.lo.u32 %2, %5, 1, %2;"
-        : "+r"(x.m), "+r"(x.h0), "+r"(x.h1)
-        : "r"(y.m), "r"(y.h0), "r"(y.h1));
-}
 
 // meta[2] <- the phase-3 chunk for this launch: halve from CHUNK3_MAX while
 // the item count (subdomains x chunks per subdomain) stays below min_items.
@@ -1326,6 +1167,18 @@ __global__ void __launch_bounds__(128) tabdiff_full_kernel(SliceDev s, const uin
 // ---------------------------------------------------------------------------
 // search batch
 // ---------------------------------------------------------------------------
+// run one search to completion; REG selects the family at compile time so a
+// kernel instantiation carries only one loop body (register pressure)
+template <int W, bool REG>
+__device__ __forceinline__ hrb::Outcome search_one(int algo, int mode, const Problem& p, uint64_t n) {
+    if (REG) {
+        hrb::Outcome o = hrb::regular_search<W>(p.a, p.b, p.eps, n);
+        if (algo == hrb::ALGO_REGULAR_UNROLLED) o.it = (o.it + 1) >> 1;
+        return o;
+    }
+    return hrb::lefevre_search<W>(p.a, p.b, p.eps, n, mode);
+}
+
 template <int W, bool REG>
 __global__ void __launch_bounds__(256) search_batch_kernel(int algo, int mode, int64_t n, const uint64_t* a,
                                                            const uint64_t* b, const uint64_t* eps,
@@ -1575,8 +1428,15 @@ int phase1_impl(Workspace& ws, const hrb_slice* s, const SliceDev& sd0, int algo
     } else {  // the classic family: lockstep pairs with refill (classic_lockstep.cuh)
         const int g5 = sm_count() * HRB_P1_MINB;
         const bool quarter = (uint64_t)s->n_total / TILE + 1 < (uint64_t)g5 * 4 * 8;
-#define P1C(WV, SHV, PLV) \
-    phase1_reg_kernel<WV, SHV, PLV, true><<<g5, 128, 0, st>>>(sd, algo, tb, bm, tt, is, tc, mode)
+#define P1C(WV, SHV, PLV)                                                                                  \
+    do {                                                                                                   \
+        if (mode == 0)                                                                                     \
+            phase1_reg_kernel<WV, SHV, PLV, 1><<<g5, 128, 0, st>>>(sd, algo, tb, bm, tt, is, tc);        \
+        else if (mode == 1)                                                                                \
+            phase1_reg_kernel<WV, SHV, PLV, 2><<<g5, 128, 0, st>>>(sd, algo, tb, bm, tt, is, tc);        \
+        else                                                                                               \
+            phase1_reg_kernel<WV, SHV, PLV, 3><<<g5, 128, 0, st>>>(sd, algo, tb, bm, tt, is, tc);        \
+    } while (0)
         if (sd.W == 64 && sd.F == 96) {
             if (quarter) P1C(64, 32, 2); else P1C(64, 32, 0);
         } else if (sd.W == 64) {
@@ -1620,15 +1480,22 @@ int phase2_impl(Workspace& ws, const hrb_slice* s, const SliceDev& sd, int algo,
             phase2_reg_kernel<32, -1><<<g4, 128, 0, st>>>(sd, split, fail_ids, fail_t, fail_count, fail_cap, mt, bm);
     } else {  // the classic family in lockstep form
         const int g4 = sm_count() * HRB_P2_MINB;
+#define P2C(WV, SHV)                                                                                         \
+    do {                                                                                                     \
+        if (mode == 0)                                                                                       \
+            phase2_reg_kernel<WV, SHV, 1><<<g4, 128, 0, st>>>(sd, split, fail_ids, fail_t, fail_count, fail_cap, mt, bm); \
+        else if (mode == 1)                                                                                  \
+            phase2_reg_kernel<WV, SHV, 2><<<g4, 128, 0, st>>>(sd, split, fail_ids, fail_t, fail_count, fail_cap, mt, bm); \
+        else                                                                                                 \
+            phase2_reg_kernel<WV, SHV, 3><<<g4, 128, 0, st>>>(sd, split, fail_ids, fail_t, fail_count, fail_cap, mt, bm); \
+    } while (0)
         if (sd.W == 64 && sd.F == 96)
-            phase2_reg_kernel<64, 32, true><<<g4, 128, 0, st>>>(sd, split, fail_ids, fail_t, fail_count, fail_cap, mt,
-                                                                bm, mode);
+            P2C(64, 32);
         else if (sd.W == 64)
-            phase2_reg_kernel<64, -1, true><<<g4, 128, 0, st>>>(sd, split, fail_ids, fail_t, fail_count, fail_cap, mt,
-                                                                bm, mode);
+            P2C(64, -1);
         else
-            phase2_reg_kernel<32, -1, true><<<g4, 128, 0, st>>>(sd, split, fail_ids, fail_t, fail_count, fail_cap, mt,
-                                                                bm, mode);
+            P2C(32, -1);
+#undef P2C
         (void)grid;
     }
     CK(cudaGetLastError());

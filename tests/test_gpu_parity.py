@@ -419,3 +419,38 @@ def test_host_path_first_call_in_fresh_process():
         os.path.abspath(__file__))), os.environ.get("PYTHONPATH", "")]))
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300, env=env)
     assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-2000:]
+
+
+@pytest.mark.parametrize("mode", [0, 1, 2])
+@pytest.mark.parametrize("algo", ["lefevre", "regular"])
+def test_phase1_iteration_sums_equal_oracle(algo, mode):
+    """The fused phase 1's SearchOutcome.iterations sum (per division mode
+    for the classic family: the batched-run counting of lowerbound.py:
+    170-222) equals the oracle cores' over the same Boolean problems, which
+    are rebuilt here from the oracle's own tabulated residues."""
+    from paper_1211_3056_b200.device import DeviceSlice, FusedRunner
+
+    batch, _ = _big_slice("exp", 1 << 40, 24, 14, algo, N=1 << 10, super_log2=16)
+    fused = FusedRunner(DeviceSlice(batch), ALGO_CODE[algo], mode, 8, sub_cap=batch.n_total * 16, cand_cap=1 << 20)
+    fused.launch()
+    r = fused.result()
+    fails, coef = oracle.phase1(batch, algo, mode, with_coeffs=True)
+    n = batch.n_total
+    t, _ = batch.locate(np.arange(n, dtype=np.uint64))
+    sizes = batch.domain_sizes(np.arange(n, dtype=np.uint64))
+    a = np.zeros(n, np.uint64)
+    b = np.zeros(n, np.uint64)
+    e = np.zeros(n, np.uint64)
+    for g in range(n):
+        s0 = int(coef[0, 0, g]) | (int(coef[0, 1, g]) << 64)
+        s1 = int(coef[1, 0, g]) | (int(coef[1, 1, g]) << 64)
+        tt = int(t[g])
+        G = int(batch.G[0, tt]) | (int(batch.G[1, tt]) << 64)
+        s2 = int(batch.s2abs[0, tt]) | (int(batch.s2abs[1, tt]) << 64)
+        a[g], b[g], e[g] = oracle.boolean_problem(s0, s1, G, s2, int(sizes[g]), batch.frac_bits, batch.word_bits)
+    ok, _, it, _, _ = oracle.search_batch(algo, mode, 1 << batch.word_bits, a, b, e, sizes)
+    if algo == "regular_unrolled":
+        it = (it + 1) // 2
+    assert np.array_equal(r.fail_ids + np.uint64(batch.id0), fails)
+    assert int((~ok.astype(bool)).sum()) == len(fails)
+    assert r.iterations == int(it.astype(np.uint64).sum()), (algo, mode)
