@@ -8,9 +8,11 @@ arguments, super-domains of 2^24 arguments (tau = 512 Taylor blocks,
 delta = 2, F = 96, L = 8), eps = 2^-32, regular search, phase-2 split 8.
 One step = the whole device hot path over the rank's slice (tabulated walk
 + Boolean tests + search + compaction, phase 2, phase 3, ordered candidate
-output): one hrb_run_slice.  The host Taylor generation (mpmath, kept on
-the host as in the paper's hybrid split) runs once before timing; its rate
-is reported separately under host_polygen.
+output): one hrb_run_slice.  The Taylor generation (native restatement of
+the reference's mpmath path, bit-identical; on the device, with the host
+library timed beside it) runs once before timing; its rate is reported
+separately under host_polygen, and end to end (generation included) under
+e2e_full.
 
     python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
@@ -92,6 +94,45 @@ def prepare_rank(args, rank, world, workers):
     return batch, time.perf_counter() - t0
 
 
+def generation_timing(args, rank, world, workers):
+    """The native generation of the rank's blocks (Taylor models, split,
+    checks, packed columns) timed both ways after one warm call each: on the
+    device (hrb_pack_blocks, what pack_plan / run_range use when CUDA is
+    there) and in the host library over `workers` threads; the two column
+    sets must be identical."""
+    import torch
+
+    from paper_1211_3056_b200 import hostgen
+    from paper_1211_3056_b200.device import pack_columns_device
+    from paper_1211_3056_b200.shard import partition_blocks
+    from paper_1211_3056_b200.slices import plan_arrays
+
+    cfg = make_cfg(args)
+    plan = plan_arrays(args.fn, 0, cfg.fmt, cfg.polygen, args.start, world << args.log2_args)
+    b0, b1 = partition_blocks(plan.sizes, world)[rank]
+    plan = plan[b0:b1]
+    hc = hostgen.make_cfg(args.fn, cfg.fmt, cfg.polygen, 0, cfg.word_bits)
+    cols = (plan.bstart, plan.bcount, plan.n_p, plan.tau, plan.e_out)
+    out = {}
+    for name, fn in (("device", lambda: pack_columns_device(hc, *cols)),
+                     ("host", lambda: hostgen.pack_columns(hc, *cols, workers))):
+        fn()
+        ts = []
+        for _ in range(3):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            res = fn()
+            torch.cuda.synchronize()
+            ts.append(time.perf_counter() - t0)
+        out[name] = (float(np.median(ts)), res, [round(1e3 * t, 3) for t in ts])
+    same = all(np.array_equal(a, b) for a, b in zip(out["device"][1], out["host"][1]))
+    n = int(plan.bcount.astype(np.uint64).sum())
+    return {"super_domains": len(plan), "device_s": out["device"][0], "host_s": out["host"][0],
+            "host_workers": workers, "device_args_per_s": n / out["device"][0], "host_args_per_s": n / out["host"][0],
+            "columns_equal": bool(same), "device_ms_samples": out["device"][2], "host_ms_samples": out["host"][2],
+            "note": "wall clock incl. plan upload and column download; pack_plan / run_range use the device"}
+
+
 def e2e_full(args, batch, workers, dist):
     """funnel.run_range over the rank's whole range, as a user calls it: block
     planning, host Taylor generation (native), packing, upload, phases 1-3,
@@ -100,6 +141,7 @@ def e2e_full(args, batch, workers, dist):
     import torch
 
     from paper_1211_3056_b200.funnel import run_range
+    from paper_1211_3056_b200.slices import DEVICE_GEN_MIN
 
     cfg = make_cfg(args)
     start, count = int(batch.m0[0]), batch.arguments
@@ -122,7 +164,8 @@ def e2e_full(args, batch, workers, dist):
     return {"seconds": float(np.median(ts)), "records": len(out.records), "intervals": len(out.interval_stats),
             "interval_args": interval, "workers": workers,
             "phase_wall_ms": {k: round(v, 3) for k, v in rows.items()},
-            "host_generation": "native (libhrbhost.so)" if batch.supers.__class__.__name__ == "PackedSupers"
+            "host_generation": "native: device (hrb_pack_blocks), host library below "
+                               f"{DEVICE_GEN_MIN} super-domains" if batch.supers.__class__.__name__ == "PackedSupers"
             else "python (mpmath)", "_records": out.records}
 
 
@@ -394,7 +437,8 @@ def main():
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     workers = max(1, (os.cpu_count() or 1) // max(1, int(os.environ.get("LOCAL_WORLD_SIZE", world))))
-    batch, prep_s = prepare_rank(args, rank, world, workers)
+    batch, _ = prepare_rank(args, rank, world, workers)
+    gen = generation_timing(args, rank, world, workers)
     count = batch.arguments
     algo = 2 if args.algo == "regular" else 0
     ds = DeviceSlice(batch)
@@ -570,8 +614,7 @@ def main():
                        "phase2_survivors": int(merged.counters[1]), "candidates": int(merged.counters[2]),
                        "gather_ms": gather_ms},
             "clocks": clocks, "gpu_launches": KERNELS_PER_STEP * args.steps, "roofline": roofline,
-            "host_polygen": {"seconds": prep_s, "workers": workers, "super_domains": batch.n_super,
-                             "args_per_s": count / prep_s},
+            "host_polygen": gen,
             "e2e": e2e, "e2e_full": full, "wide": wide}
     if not args.no_cpu_baseline and world == 1:  # rank 0 at N=1 only
         cb = cpu_baseline(args, batch, args.cpu_seconds)

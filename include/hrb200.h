@@ -16,6 +16,8 @@
 
 #include <stdint.h>
 
+#include "hrb_host.h" /* hrbh_cfg (hrb_pack_blocks) */
+
 #ifdef __cplusplus
 extern "C" {
 #endif
@@ -272,6 +274,22 @@ int hrb_wdomain_coefficients(const hrb_wslice* s, uint32_t* out, void* stream);
  */
 int hrb_confirm_exp(int precision, int eps_bits, int binade, int64_t n, const uint64_t* index, uint8_t* is_hr,
                     uint64_t* dist_raw, uint8_t* status, void* stream);
+
+/*
+ * Native generation on the device: hrbh_pack_blocks (include/hrb_host.h --
+ * Taylor model, split, checks and packed columns of S super-domains, the
+ * reference's polygen.py:193-280 and slices.check_super) with one device
+ * thread per super-domain running the same source (csrc/host/polygen.h),
+ * bit-identical to the host library.  Outputs as hrbh_pack_blocks: coef
+ * uint32[6][limbs + 1][S], G / s2abs uint64[2][S], status[t] (HRBH_OK or
+ * HRBH_FALLBACK: the exact Python path takes the item), shift_ok[t].
+ * Configuration domain: the host library's, with limbs <= 12 and
+ * frac_bits + guard <= 224 (the device's fixed 1024-bit capacity);
+ * HRB_ERR_CONFIG otherwise.  All array pointers are device pointers.
+ */
+int hrb_pack_blocks(const hrbh_cfg* cfg, int64_t S, const uint64_t* index_start, const uint64_t* count,
+                    const uint32_t* n_p, const uint32_t* tau, const int32_t* e_out, uint32_t* coef, uint64_t* G,
+                    uint64_t* s2abs, uint8_t* status, uint8_t* shift_ok, void* stream);
 
 #ifdef __cplusplus
 }

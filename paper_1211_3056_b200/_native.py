@@ -38,6 +38,7 @@ EXPORTS = (
     "hrb_wrun_slice_host",
     "hrb_wdomain_coefficients",
     "hrb_confirm_exp",
+    "hrb_pack_blocks",
 )
 
 
@@ -126,6 +127,7 @@ def _declare(lib) -> None:
     lib.hrb_wrun_slice_host.argtypes = [C.POINTER(HrbWSlice), I, I, P, P, P, P, U64, C.POINTER(C.c_float)]
     lib.hrb_wdomain_coefficients.argtypes = [C.POINTER(HrbWSlice), P, P]
     lib.hrb_confirm_exp.argtypes = [I, I, I, I64, P, P, P, P, P]
+    lib.hrb_pack_blocks.argtypes = [P, I64, P, P, P, P, P, P, P, P, P, P, P]
     for name in EXPORTS:
         if name not in ("hrb_version", "hrb_last_error"):
             getattr(lib, name).restype = I

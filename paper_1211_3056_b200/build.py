@@ -24,13 +24,13 @@ SOURCES = [os.path.join(CSRC, "hrb200.cu")]
 PEAK_SOURCES = [os.path.join(CSRC, "intpeak.cu")]
 HOST_LIB = os.path.join(LIBDIR, "libhrbhost.so")  # native host polygen + confirmation (no CUDA)
 HOST_SOURCES = [os.path.join(CSRC, "host", "hrb_host.cpp")]
-HOST_HEADERS = [os.path.join(CSRC, "host", f) for f in ("bign.h", "mpexp.h", "decide.h")] + [
+HOST_HEADERS = [os.path.join(CSRC, "host", f) for f in ("bign.h", "mpexp.h", "decide.h", "polygen.h")] + [
     os.path.join(ROOT, "include", "hrb_host.h")]
 HOST_FLAGS = ["-O3", "-std=c++17", "-fopenmp", "-fPIC", "-shared", "-Wall", "-Wextra", "-Wno-unused-parameter",
               "-Wno-maybe-uninitialized"]
 HEADERS = [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC)) if f.endswith((".cuh", ".h"))] + [
-    os.path.join(CSRC, "host", f) for f in ("bign.h", "mpexp.h", "decide.h")] + [
-    os.path.join(ROOT, "include", "hrb200.h")]
+    os.path.join(CSRC, "host", f) for f in ("bign.h", "mpexp.h", "decide.h", "polygen.h")] + [
+    os.path.join(ROOT, "include", f) for f in ("hrb200.h", "hrb_host.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -33,6 +33,7 @@
 
 #include "../../include/hrb200.h"
 #include "confirm.cuh"
+#include "host/polygen.h"
 #include "search_core.cuh"
 #include "tile_search.cuh"
 #include "classic_lockstep.cuh"
@@ -2211,6 +2212,70 @@ extern "C" int hrb_confirm_exp(int precision, int eps_bits, int binade, int64_t 
     else if (nl == 6) FAST(6);
     else confirm_exp_kernel<<<grid, 128, 0, st>>>(precision, eps_bits, binade, n, index, is_hr, dist_raw, status);
 #undef FAST
+    CK(cudaGetLastError());
+    return HRB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// native generation on the device: one thread per super-domain runs
+// csrc/host/polygen.h's one_block -- the SAME source as libhrbhost.so's
+// hrbh_pack_blocks -- and writes the packed columns in place
+// ---------------------------------------------------------------------------
+#ifndef HRB_GEN_MINB
+#define HRB_GEN_MINB 8
+#endif
+__global__ void __launch_bounds__(64, HRB_GEN_MINB) pack_blocks_kernel(hrbh_cfg c, int64_t S, const uint64_t* index_start,
+                                                         const uint64_t* count, const uint32_t* n_p,
+                                                         const uint32_t* tau, const int32_t* e_out, uint32_t* coef,
+                                                         uint64_t* G, uint64_t* s2abs, uint8_t* status,
+                                                         uint8_t* shift_ok) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= S) return;
+    hrbh::BlockOut o;
+    if (!hrbh::one_block(c, index_start[t], count[t], n_p[t], tau[t], e_out[t], &o)) {
+        status[t] = HRBH_FALLBACK;
+        return;
+    }
+    const int cl = c.limbs + 1;
+    status[t] = HRBH_OK;
+    shift_ok[t] = o.shift_ok ? 1 : 0;
+    for (int k = 0; k < 6; k++) hrbh::put_limbs(o.r[k], cl, coef, k, S, t);
+    G[t] = o.G.n > 0 ? o.G.w[0] : 0;
+    G[S + t] = o.G.n > 1 ? o.G.w[1] : 0;
+    s2abs[t] = o.s2.n > 0 ? o.s2.w[0] : 0;
+    s2abs[S + t] = o.s2.n > 1 ? o.s2.w[1] : 0;
+}
+
+extern "C" int hrb_pack_blocks(const hrbh_cfg* cfg, int64_t S, const uint64_t* index_start, const uint64_t* count,
+                               const uint32_t* n_p, const uint32_t* tau, const int32_t* e_out, uint32_t* coef,
+                               uint64_t* G, uint64_t* s2abs, uint8_t* status, uint8_t* shift_ok, void* stream) {
+    // the host library's configuration domain, with the device's fixed
+    // capacity (1024-bit values, hrbh::NW): limbs <= 12 keeps every product
+    // of the checks below 2^1024, frac_bits + guard <= 224 the enclosures'
+    // squarings (wp <= 270)
+    if (!cfg || cfg->fn != HRBH_FN_EXP || cfg->precision < 2 || cfg->precision > 64 || cfg->eps_bits < 1 ||
+        cfg->binade > 0 || cfg->binade <= -1000 || cfg->frac_bits < 8 || cfg->guard < 0 || cfg->limbs < 1 ||
+        cfg->limbs > 12 || cfg->frac_bits + cfg->guard > 224 || (cfg->delta != 1 && cfg->delta != 2) ||
+        (cfg->word_bits != 32 && cfg->word_bits != 64) || S < 0)
+        return set_err(HRB_ERR_CONFIG, "hrb_pack_blocks: exp on binades <= 0, delta <= 2, limbs <= 12, "
+                                       "frac_bits + guard <= 224");
+    if (S == 0) return HRB_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    // The kernel keeps ~15 KB of big integers per thread in local memory.
+    // Raising the stack limit to that once keeps the driver's local-memory
+    // reservation in place between launches (left to itself, the driver
+    // may shrink it after a launch and grow it again, ~5 ms, on the next).
+    static std::once_flag stack_once;
+    std::call_once(stack_once, [] {
+        cudaFuncAttributes fa;
+        size_t cur = 0;
+        if (cudaFuncGetAttributes(&fa, pack_blocks_kernel) == cudaSuccess &&
+            cudaDeviceGetLimit(&cur, cudaLimitStackSize) == cudaSuccess && cur < fa.localSizeBytes)
+            cudaDeviceSetLimit(cudaLimitStackSize, fa.localSizeBytes);
+        cudaGetLastError();
+    });
+    pack_blocks_kernel<<<(unsigned)((S + 63) / 64), 64, 0, st>>>(*cfg, S, index_start, count, n_p, tau, e_out, coef,
+                                                                G, s2abs, status, shift_ok);
     CK(cudaGetLastError());
     return HRB_OK;
 }

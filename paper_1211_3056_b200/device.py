@@ -357,3 +357,31 @@ def search_verdict_arrays(algo_code: int, word_bits: int, a, b, eps, count, devi
                                                              nat.stream_ptr()))
     torch.cuda.synchronize()
     return ok[:n].cpu().numpy(), _u64(d[:n]), _u64(it[:n])
+
+
+def pack_columns_device(cfg, index_start, count, n_p, tau, e_out, device=None):
+    """hrb_pack_blocks: the native generation (hostgen.pack_columns' Taylor
+    models, split, checks and packed columns) with one device thread per
+    super-domain, the same source as the host library.  Returns host numpy
+    arrays (coef, G, s2abs, status, shift_ok) like hostgen.pack_columns."""
+    torch = nat.require_cuda()
+    lib = nat.load()
+    dev = device or torch.device("cuda", torch.cuda.current_device())
+    S = len(index_start)
+    cl = cfg.limbs + 1
+
+    def up(a, dt, view):
+        return torch.from_numpy(np.ascontiguousarray(a, dtype=dt).view(view)).to(dev, non_blocking=False)
+
+    ins = [up(index_start, np.uint64, np.int64), up(count, np.uint64, np.int64), up(n_p, np.uint32, np.int32),
+           up(tau, np.uint32, np.int32), up(e_out, np.int32, np.int32)]
+    coef = torch.zeros((6, cl, S), dtype=torch.int32, device=dev)
+    G = torch.zeros((2, S), dtype=torch.int64, device=dev)
+    s2 = torch.zeros((2, S), dtype=torch.int64, device=dev)
+    status = torch.zeros(S, dtype=torch.uint8, device=dev)
+    ok2 = torch.zeros(S, dtype=torch.uint8, device=dev)
+    nat.check("hrb_pack_blocks", lib.hrb_pack_blocks(C.byref(cfg), S, *(t.data_ptr() for t in ins), coef.data_ptr(),
+                                                     G.data_ptr(), s2.data_ptr(), status.data_ptr(), ok2.data_ptr(),
+                                                     nat.stream_ptr()))
+    return (coef.cpu().numpy().view(np.uint32), G.cpu().numpy().view(np.uint64), s2.cpu().numpy().view(np.uint64),
+            status.cpu().numpy(), ok2.cpu().numpy())

@@ -535,16 +535,33 @@ class PackedSupers:
         return (self[i] for i in range(len(self)))
 
 
+DEVICE_GEN_MIN = 256  # super-domains from which the device generation pays for its launch and copies
+
+
+def _device_gen_ok(pg: PolyGenConfig, n: int) -> bool:
+    if n < DEVICE_GEN_MIN or pg.limbs > 12 or pg.frac_bits + pg.guard > 224:
+        return False
+    try:
+        import torch
+
+        return torch.cuda.is_available()
+    except Exception:  # pragma: no cover
+        return False
+
+
 def pack_plan(plan: BlockPlan, word_bits: int, budget_ceiling: Fraction | None = None,
-              workers: int = 1, native: bool | None = None) -> SliceBatch:
+              workers: int = 1, native: bool | None = None, device: bool | None = None) -> SliceBatch:
     """Taylor models + split + checks + packing of planned blocks.
 
-    With the native host library (hostgen: exp on binades <= 0, delta <= 2,
-    no budget ceiling) every block runs in C++ over `workers` host threads,
-    bit-identical to the Python path; blocks it flags go through the exact
-    Python path one by one (raising the reference's error where the
-    reference raises).  native=False forces the Python path; otherwise the
-    native path runs wherever it covers the configuration."""
+    With the native generation (exp on binades <= 0, delta <= 2, no budget
+    ceiling) every block runs in compiled code, bit-identical to the Python
+    path: on the GPU (hrb_pack_blocks, one thread per block) when CUDA is
+    there and the slice has DEVICE_GEN_MIN blocks or more (device=True /
+    False forces the choice), else in libhrbhost.so over `workers` host
+    threads.  Blocks it flags go through the exact Python path one by one
+    (raising the reference's error where the reference raises).
+    native=False forces the Python path; otherwise the native path runs
+    wherever it covers the configuration."""
     from . import hostgen
 
     fmt, pg = plan.fmt, plan.pg
@@ -559,8 +576,15 @@ def pack_plan(plan: BlockPlan, word_bits: int, budget_ceiling: Fraction | None =
         return pack_slice(supers_of_blocks(blocks, workers), fmt, pg, word_bits, plan.binade,
                           budget_ceiling=budget_ceiling, workers=workers)
     cfg = hostgen.make_cfg(plan.fn, fmt, pg, plan.binade, word_bits)
-    coef, G, s2, status, ok2 = hostgen.pack_columns(cfg, plan.bstart, plan.bcount, plan.n_p, plan.tau, plan.e_out,
-                                                    workers)
+    if device is None:
+        device = _device_gen_ok(pg, len(plan))
+    if device:
+        from .device import pack_columns_device
+
+        coef, G, s2, status, ok2 = pack_columns_device(cfg, plan.bstart, plan.bcount, plan.n_p, plan.tau, plan.e_out)
+    else:
+        coef, G, s2, status, ok2 = hostgen.pack_columns(cfg, plan.bstart, plan.bcount, plan.n_p, plan.tau,
+                                                        plan.e_out, workers)
     for t in np.flatnonzero(status != hostgen.HRBH_OK).tolist():
         sd = _make_super(plan.block(t))  # exact Python path; raises where the reference raises
         c1, g1, s21, _, k1 = _pack_rows([sd], fmt, pg, word_bits, budget_ceiling, True)

@@ -1,0 +1,88 @@
+"""Native generation on the device (hrb_pack_blocks): one GPU thread per
+super-domain runs csrc/host/polygen.h, the same source as libhrbhost.so's
+hrbh_pack_blocks.  Pinned to the reference's own fixtures (the packed
+super-domains the reference computed) and, column for column, to the host
+library on random configurations, fallback flags included."""
+import random
+
+import numpy as np
+import pytest
+
+from golden_io import batch_of, case, config_of, pipeline_cases
+
+from paper_1211_3056_b200 import hostgen, slices
+from paper_1211_3056_b200.fpformat import FpFormat
+from paper_1211_3056_b200.taylor import PolyGenConfig
+
+pytestmark = pytest.mark.gpu
+
+PACKED = ("coef", "G", "s2abs", "n_dom", "dom_n", "last_n", "dom_base", "m0")
+
+
+@pytest.mark.parametrize("name", [c["name"] for c in pipeline_cases() if c["fn"] == "exp" and c["binade"] <= 0])
+def test_device_pack_equals_reference_fixture(name):
+    c = case(name)
+    cfg = config_of(c)
+    want = batch_of(c)
+    start, count = c["slice"]
+    plan = slices.plan_arrays(c["fn"], c["binade"], cfg.fmt, cfg.polygen, start, count)
+    got = slices.pack_plan(plan, cfg.word_bits, workers=1, native=True, device=True)
+    for k in PACKED:
+        assert np.array_equal(getattr(got, k), getattr(want, k)), k
+    assert np.array_equal(got.shift_bound_ok, want.shift_bound_ok)
+
+
+def _random_plan(rng):
+    p = rng.choice([24, 32, 53, 53, 64])
+    eps_bits = rng.randint(8, 40)
+    fmt = FpFormat(p, eps_bits)
+    N = 1 << rng.randint(6, 15)
+    tau = 1 << rng.randint(1, 9)
+    mu = 1 << rng.randint(0, tau.bit_length() - 1)
+    delta = rng.choice([1, 2, 2])
+    F = rng.choice([48, 64, 96, 112, 128])
+    W = rng.choice([32, 64]) if F >= 64 else 32
+    pg = PolyGenConfig(tau=tau, N=N, mu=mu, nu=tau // mu, delta=delta, limbs=rng.randint(2, 12), frac_bits=F,
+                       guard=rng.choice([0, 8, 32, 64]))
+    binade = rng.choice([0, 0, -1, -7, -60])
+    span = 1 << (p - 1)
+    count = min(span, rng.randint(1, 1 << 12) * N * tau // rng.choice([1, 3, 7]))
+    start = rng.randrange(0, span - count + 1)
+    return slices.plan_arrays("exp", binade, fmt, pg, start, count), fmt, pg, binade, W
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_device_columns_equal_host_library(seed):
+    from paper_1211_3056_b200.device import pack_columns_device
+
+    rng = random.Random(7000 + seed)
+    plan, fmt, pg, binade, W = _random_plan(rng)
+    if not len(plan):
+        pytest.skip("empty plan")
+    cfg = hostgen.make_cfg("exp", fmt, pg, binade, W)
+    cols = (plan.bstart, plan.bcount, plan.n_p, plan.tau, plan.e_out)
+    host = hostgen.pack_columns(cfg, *cols, 1)
+    dev = pack_columns_device(cfg, *cols)
+    for name, h, d in zip(("coef", "G", "s2abs", "status", "shift_ok"), host, dev):
+        if name in ("coef", "G", "s2abs", "shift_ok"):  # fallback columns are unspecified
+            ok = host[3] == hostgen.HRBH_OK
+            h, d = h[..., ok], d[..., ok]
+        assert np.array_equal(h, d), (seed, name)
+
+
+def test_device_columns_at_2p36():
+    """4,096 super-domains (the C4/C5 slice size) and the 2^40 bench slice's
+    first 8,192 blocks: device == host library."""
+    from paper_1211_3056_b200.device import pack_columns_device
+
+    fmt = FpFormat(53, 32)
+    pg = PolyGenConfig(tau=512, N=1 << 15, mu=16, nu=32, delta=2, limbs=8, frac_bits=96, guard=32)
+    for start, count in ((0, 1 << 36), (1 << 45, 1 << 37)):
+        plan = slices.plan_arrays("exp", 0, fmt, pg, start, count)
+        cfg = hostgen.make_cfg("exp", fmt, pg, 0, 64)
+        cols = (plan.bstart, plan.bcount, plan.n_p, plan.tau, plan.e_out)
+        host = hostgen.pack_columns(cfg, *cols, 0)
+        dev = pack_columns_device(cfg, *cols)
+        assert (host[3] == hostgen.HRBH_OK).all()
+        for h, d in zip(host, dev):
+            assert np.array_equal(h, d)
