@@ -145,7 +145,7 @@ def e2e_full(args, batch, workers, dist):
 
     cfg = make_cfg(args)
     start, count = int(batch.m0[0]), batch.arguments
-    interval = 1 << min(args.log2_args, 38)
+    interval = 1 << min(args.log2_args, 40)  # one interval per 2^40 (generation on the device)
     run = lambda: run_range(args.fn, 0, start, count, cfg, interval_args=interval, workers=workers)  # noqa: E731
     out = run()
     ts = []

@@ -18,6 +18,8 @@ reference would have rejected.
 
 from __future__ import annotations
 
+import functools
+
 import math
 import os
 from dataclasses import dataclass, field
@@ -62,6 +64,13 @@ class SuperDomain:
 def output_binade_pieces(fn: str, binade: int, fmt: FpFormat) -> list[tuple[int, int, int]]:
     """Maximal runs (start, count, e_out) of constant output exponent over
     the binade's argument indices (pipeline.py:296-347)."""
+    return list(_output_binade_pieces(fn, binade, fmt))
+
+
+@functools.lru_cache(maxsize=256)
+def _output_binade_pieces(fn: str, binade: int, fmt: FpFormat) -> tuple[tuple[int, int, int], ...]:
+    # a pure function of its arguments (rigorous exponent enclosures), planned
+    # once per (fn, binade, format) instead of once per slice / interval
     count = 1 << (fmt.precision - 1)
     base = Domain(1 << (fmt.precision - 1), binade + 1, count)
 
@@ -81,7 +90,7 @@ def output_binade_pieces(fn: str, binade: int, fmt: FpFormat) -> list[tuple[int,
                 run_start, run_e = i, e_i
         if run_e is not None:
             pieces.append((run_start, count - run_start, run_e))
-        return pieces
+        return tuple(pieces)
     start = 1 if (fn == "log" and binade == 0) else 0
     pieces = []
     while start < count:
@@ -98,7 +107,7 @@ def output_binade_pieces(fn: str, binade: int, fmt: FpFormat) -> list[tuple[int,
                 hi = mid - 1
         pieces.append((start, lo - start + 1, e0))
         start = lo + 1
-    return pieces
+    return tuple(pieces)
 
 
 def piece_domain_size(fn: str, piece: Domain, e_out: int, fmt: FpFormat, n_max: int) -> int:

@@ -14,6 +14,12 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:"pha
    -o gpurun_out/prof_full_$T -f python scripts/profile_step.py --no-peak > gpurun_out/ncu_full_$T.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"phase1_wide|phase2_wide|phase3_wide|wseed" -c 4 \
    -o gpurun_out/prof_wide_$T -f python scripts/wide_probe.py --deltas 4 --steps 1 > gpurun_out/ncu_wide_$T.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"phase1_reg" -c 1 \
+   -o gpurun_out/prof_classic_$T -f python scripts/profile_step.py --no-peak --algo lefevre > gpurun_out/ncu_classic_$T.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"pack_blocks" -c 1 \
+   -o gpurun_out/prof_gen_$T -f python scripts/devgen_probe.py > gpurun_out/ncu_gen_$T.log 2>&1
+timeout 300 python scripts/devgen_probe.py > gpurun_out/devgen_$T.json 2> gpurun_out/devgen_$T.err
+timeout 600 python scripts/e2e_full_probe.py --interval 40 > gpurun_out/e2e_full_probe_$T.json 2> gpurun_out/e2e_full_probe_$T.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
    --log-file gpurun_out/launches_$T.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-e2e-full --wide-delta 0 > gpurun_out/ncu_launch_$T.log 2>&1
 timeout 900 python scripts/bench_search.py --verdicts > gpurun_out/bench_search_$T.json 2> gpurun_out/bench_search_$T.err
