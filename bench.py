@@ -94,7 +94,7 @@ def prepare_rank(args, rank, world, workers):
     return batch, time.perf_counter() - t0
 
 
-def generation_timing(args, rank, world, workers):
+def generation_timing(args, rank, world, workers, prep_s):
     """The native generation of the rank's blocks (Taylor models, split,
     checks, packed columns) timed both ways after one warm call each: on the
     device (hrb_pack_blocks, what pack_plan / run_range use when CUDA is
@@ -111,6 +111,9 @@ def generation_timing(args, rank, world, workers):
     plan = plan_arrays(args.fn, 0, cfg.fmt, cfg.polygen, args.start, world << args.log2_args)
     b0, b1 = partition_blocks(plan.sizes, world)[rank]
     plan = plan[b0:b1]
+    if not hostgen.covers(args.fn, 0, cfg.fmt, cfg.polygen):
+        return {"super_domains": len(plan), "path": f"python (mpmath): {args.fn} is not covered by the native "
+                "generation", "seconds": prep_s, "host_workers": workers}
     hc = hostgen.make_cfg(args.fn, cfg.fmt, cfg.polygen, 0, cfg.word_bits)
     cols = (plan.bstart, plan.bcount, plan.n_p, plan.tau, plan.e_out)
     out = {}
@@ -437,8 +440,8 @@ def main():
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     workers = max(1, (os.cpu_count() or 1) // max(1, int(os.environ.get("LOCAL_WORLD_SIZE", world))))
-    batch, _ = prepare_rank(args, rank, world, workers)
-    gen = generation_timing(args, rank, world, workers)
+    batch, prep_s = prepare_rank(args, rank, world, workers)
+    gen = generation_timing(args, rank, world, workers, prep_s)
     count = batch.arguments
     algo = 2 if args.algo == "regular" else 0
     ds = DeviceSlice(batch)

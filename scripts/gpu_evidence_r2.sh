@@ -34,3 +34,13 @@ HRB_BENCH_ONE_DEVICE=1 timeout 900 python -m torch.distributed.run --nnodes=1 --
   --master-port 29531 bench.py --gpus 2 --steps 3 --warmup 3 --log2-args 36 --no-e2e --wide-delta 0 > gpurun_out/multirank2_$T.json 2> gpurun_out/multirank2_$T.err
 echo "multirank rc=$?"
 tail -n 3 gpurun_out/pytest_gpu_$T.log gpurun_out/smoke_$T.log
+# keep the merge-back under 64 MiB: the captures as CSV pages, not .ncu-rep
+for rep in gpurun_out/prof_*_$T.ncu-rep; do
+  [ -f "$rep" ] || continue
+  b=${rep%.ncu-rep}
+  ncu -i "$rep" --page raw --csv > "${b}_raw.csv" 2>/dev/null
+  ncu -i "$rep" --page source --csv --print-source sass > "${b}_src.csv" 2>/dev/null
+  gzip -f "${b}_src.csv"
+  rm -f "$rep"
+done
+du -sh gpurun_out
