@@ -359,6 +359,9 @@ def search_verdict_arrays(algo_code: int, word_bits: int, a, b, eps, count, devi
     return ok[:n].cpu().numpy(), _u64(d[:n]), _u64(it[:n])
 
 
+PIN_GEN_MIN = 8192  # super-domains from which pack_columns_device downloads into pinned memory
+
+
 def pack_columns_device(cfg, index_start, count, n_p, tau, e_out, device=None):
     """hrb_pack_blocks: the native generation (hostgen.pack_columns' Taylor
     models, split, checks and packed columns) with one device thread per
@@ -383,5 +386,17 @@ def pack_columns_device(cfg, index_start, count, n_p, tau, e_out, device=None):
     nat.check("hrb_pack_blocks", lib.hrb_pack_blocks(C.byref(cfg), S, *(t.data_ptr() for t in ins), coef.data_ptr(),
                                                      G.data_ptr(), s2.data_ptr(), status.data_ptr(), ok2.data_ptr(),
                                                      nat.stream_ptr()))
-    return (coef.cpu().numpy().view(np.uint32), G.cpu().numpy().view(np.uint64), s2.cpu().numpy().view(np.uint64),
-            status.cpu().numpy(), ok2.cpu().numpy())
+    # download into pinned host memory (torch's caching host allocator): a
+    # pageable download of the 16 MB of a 2^40 slice runs at a few GB/s once
+    # it has to fault in fresh pages, and the pinned columns also make the
+    # later upload of the slice a direct DMA
+    # (small slices: pageable; pinning fresh host memory costs more than it saves)
+    pin = S >= PIN_GEN_MIN
+    outs = []
+    for t in (coef, G, s2, status, ok2):
+        h = torch.empty(t.shape, dtype=t.dtype, pin_memory=pin)
+        h.copy_(t, non_blocking=pin)
+        outs.append(h)
+    torch.cuda.current_stream(dev).synchronize()
+    return (outs[0].numpy().view(np.uint32), outs[1].numpy().view(np.uint64), outs[2].numpy().view(np.uint64),
+            outs[3].numpy(), outs[4].numpy())
