@@ -285,7 +285,10 @@ int hrb_confirm_exp(int precision, int eps_bits, int binade, int64_t n, const ui
  * HRBH_FALLBACK: the exact Python path takes the item), shift_ok[t].
  * Configuration domain: the host library's, with limbs <= 12 and
  * frac_bits + guard <= 224 (the device's fixed 1024-bit capacity);
- * HRB_ERR_CONFIG otherwise.  All array pointers are device pointers.
+ * HRB_ERR_CONFIG otherwise.  All array pointers are device pointers.  The
+ * kernel keeps ~15 KB of big integers per thread in local memory, which the
+ * driver reserves for every resident thread (~4.2 GB on a B200) from the
+ * first call on.
  */
 int hrb_pack_blocks(const hrbh_cfg* cfg, int64_t S, const uint64_t* index_start, const uint64_t* count,
                     const uint32_t* n_p, const uint32_t* tau, const int32_t* e_out, uint32_t* coef, uint64_t* G,

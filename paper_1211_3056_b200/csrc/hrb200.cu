@@ -2261,19 +2261,9 @@ extern "C" int hrb_pack_blocks(const hrbh_cfg* cfg, int64_t S, const uint64_t* i
                                        "frac_bits + guard <= 224");
     if (S == 0) return HRB_OK;
     cudaStream_t st = (cudaStream_t)stream;
-    // The kernel keeps ~15 KB of big integers per thread in local memory.
-    // Raising the stack limit to that once keeps the driver's local-memory
-    // reservation in place between launches (left to itself, the driver
-    // may shrink it after a launch and grow it again, ~5 ms, on the next).
-    static std::once_flag stack_once;
-    std::call_once(stack_once, [] {
-        cudaFuncAttributes fa;
-        size_t cur = 0;
-        if (cudaFuncGetAttributes(&fa, pack_blocks_kernel) == cudaSuccess &&
-            cudaDeviceGetLimit(&cur, cudaLimitStackSize) == cudaSuccess && cur < fa.localSizeBytes)
-            cudaDeviceSetLimit(cudaLimitStackSize, fa.localSizeBytes);
-        cudaGetLastError();
-    });
+    // The kernel keeps ~15 KB of big integers per thread in local memory;
+    // the driver reserves that for every resident thread slot (~4.2 GB of
+    // device memory on a B200, kept after the first launch).
     pack_blocks_kernel<<<(unsigned)((S + 63) / 64), 64, 0, st>>>(*cfg, S, index_start, count, n_p, tau, e_out, coef,
                                                                 G, s2abs, status, shift_ok);
     CK(cudaGetLastError());
