@@ -369,7 +369,10 @@ def pack_columns_device(cfg, index_start, count, n_p, tau, e_out, device=None):
     arrays (coef, G, s2abs, status, shift_ok) like hostgen.pack_columns."""
     torch = nat.require_cuda()
     lib = nat.load()
-    dev = device or torch.device("cuda", torch.cuda.current_device())
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    if dev.index is not None and dev.index != torch.cuda.current_device():
+        with torch.cuda.device(dev):  # the library launches on the current device's stream
+            return pack_columns_device(cfg, index_start, count, n_p, tau, e_out, dev)
     S = len(index_start)
     cl = cfg.limbs + 1
 

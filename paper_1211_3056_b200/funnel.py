@@ -276,6 +276,16 @@ def _confirm_native(fn: str, cand: list, fmt: FpFormat, workers: int):
 DEVICE_CONFIRM_MIN = 4096  # candidates from which the device confirmation pays for its copies
 
 
+def _current_cuda_device():
+    """The calling thread's CUDA device index, or None without CUDA."""
+    try:
+        import torch
+
+        return torch.cuda.current_device() if torch.cuda.is_available() else None
+    except Exception:  # pragma: no cover
+        return None
+
+
 def _cuda_ready() -> bool:
     try:
         import torch
@@ -545,7 +555,16 @@ def run_range(fn: str, binade: int, start: int, count: int, cfg: PipelineConfig,
     ceiling = cfg.phase.budgets.eps_dprime if cfg.phase.budgets is not None else None
     bstart_of = [int(plan.bstart[p[0]]) for p in parts]
 
+    # the generation runs in a worker thread: give it the caller's CUDA device
+    # (a new thread starts on device 0, which under torchrun is another
+    # rank's GPU)
+    dev = _current_cuda_device()
+
     def prepare(part):
+        if dev is not None:
+            import torch
+
+            torch.cuda.set_device(dev)
         if wide is not None:
             return pack_wide(plan[part[0]:part[1]], wide, w)
         return pack_plan(plan[part[0]:part[1]], cfg.word_bits, budget_ceiling=ceiling, workers=w, native=native)
