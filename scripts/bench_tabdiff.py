@@ -53,6 +53,23 @@ def main():
         torch.cuda.synchronize()
         ms.append(e0.elapsed_time(e1))
     t = float(np.mean(ms))
+    # the write-only ceiling of this device: torch fills of 1 GiB (the kernel
+    # is store-bound; the copy peak in MEASURED_PEAKS.json counts reads too)
+    fills = {}
+    big = torch.empty(1 << 28, dtype=torch.int32, device="cuda")
+    for name, fn in (("fill_i32", lambda: big.fill_(7)), ("zero_i32", lambda: big.zero_())):
+        for _ in range(3):
+            fn()
+        ts = []
+        for _ in range(10):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        fills[name] = (1 << 30) / (min(ts) / 1e3) / 1e9
+    wo = max(fills.values())
     written = out.numel() * 4
     read = batch.coef.nbytes + batch.n_dom.nbytes + batch.dom_base.nbytes
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs")
@@ -61,6 +78,7 @@ def main():
                       "limbs": cl, "ms": t, "domains_per_s": batch.n_total / (t / 1e3),
                       "args_per_s": batch.arguments / (t / 1e3), "bytes_written": written, "bytes_read": read,
                       "achieved_gbs": gbs, "peak_gbs": peak, "frac": gbs / peak if peak else None,
+                      "write_only_gbs": wo, "write_only_probes": fills, "frac_of_write_only": gbs / wo,
                       "note": "includes the per-launch prep kernels (tile scan); L2 flushed before each launch"}))
 
 
