@@ -86,3 +86,27 @@ def test_device_columns_at_2p36():
         assert (host[3] == hostgen.HRBH_OK).all()
         for h, d in zip(host, dev):
             assert np.array_equal(h, d)
+
+
+@pytest.mark.parametrize("seed", [6, 14, 21, 25, 28, 32, 35, 38, 1, 9])
+def test_pack_plan_device_raises_like_host(seed):
+    """pack_plan on the device hands the blocks it flags to the exact Python
+    path, which raises the reference's error where the reference raises
+    (MPOverflowError here) -- the same exception and message as the host
+    library's pack_plan -- and otherwise returns the same slice."""
+    rng = random.Random(7000 + seed)
+    plan, fmt, pg, binade, W = _random_plan(rng)
+
+    def run(device):
+        try:
+            return slices.pack_plan(plan, W, workers=1, native=True, device=device), None
+        except Exception as exc:  # noqa: BLE001 - compared below
+            return None, (type(exc).__name__, str(exc))
+
+    got, gerr = run(True)
+    want, werr = run(False)
+    assert gerr == werr
+    if want is not None:
+        for k in PACKED:
+            assert np.array_equal(getattr(got, k), getattr(want, k)), k
+        assert np.array_equal(got.shift_bound_ok, want.shift_bound_ok)
