@@ -34,8 +34,6 @@ namespace hrb {
 struct Slot {
     uint64_t A, B, d;
     float Af, Bf;
-    float df;  // float(d), kept for the d-reduction's estimate when HRB_DF (see hs_fast)
-    float rn;  // HRB_RCPN: 1 / float(next half-step's divisor), issued a half-step early
     uint32_t cA, cB, M;
 };
 
@@ -72,23 +70,6 @@ __device__ __forceinline__ uint64_t sub_nb(uint64_t x, uint64_t y, bool& ge) {
 
 constexpr int32_t QMAX = 1 << 20;
 
-// HRB_DF: the d-reduction's quotient estimate reads a float of d kept in the
-// slot (rounded once per half-step, off the critical path) and, on an
-// else-half, float(d) - float(r) instead of float(d - r): the estimate no
-// longer waits for the exact 64-bit subtraction and its select.  Its error
-// grows to ~2^-24 (d + r) / S < 2^-24 (k + 2), still below 1 for k < 2^20,
-// so a wrong estimate is off by one and the exact y < S check catches it.
-#ifndef HRB_DF
-#define HRB_DF 0
-#endif
-
-// HRB_RCPN: the reciprocal of a half-step's divisor is issued by the
-// half-step that produced that divisor (right after its float rounding, so
-// the MUFU latency overlaps the vote and the commit) and kept in the slot.
-#ifndef HRB_RCPN
-#define HRB_RCPN 0
-#endif
-
 // x + k * y mod 2^64 for a 32-bit k.  With y = -S precomputed once per
 // half-step, both of its products (L - k S and x - k2 S) compile to one wide
 // multiply-add on the low word and one multiply-add on the high word.
@@ -110,9 +91,9 @@ __device__ __forceinline__ uint64_t madd64(uint64_t x, uint32_t k, uint64_t y) {
 // estimate is clamped at 0 and a wrapped subtraction is caught directly
 // (result above its minuend), since ">= S" no longer implies a wrap there.
 template <bool THEN, bool FIRST = false>
-__device__ __forceinline__ void hs_fast(uint64_t& L, uint64_t S, float& Lf, float Sf, uint64_t& d, float& df,
-                                        float& rn, uint32_t& k, uint32_t& k2, bool& sub, bool& bad) {
-    const float rcp = HRB_RCPN ? rn : rcp_approx(Sf);
+__device__ __forceinline__ void hs_fast(uint64_t& L, uint64_t S, float& Lf, float Sf, uint64_t& d, uint32_t& k,
+                                        uint32_t& k2, bool& sub, bool& bad) {
+    const float rcp = rcp_approx(Sf);
     // floor(L/S) >= 1 except on a first step, so the estimate is >= 0
     const int32_t ke = FIRST ? max(qfloor(Lf, rcp), 0) : qfloor(Lf, rcp);
     const uint64_t nS = 0 - S;
@@ -124,21 +105,11 @@ __device__ __forceinline__ void hs_fast(uint64_t& L, uint64_t S, float& Lf, floa
         const uint64_t t = sub_nb(d, r, sub);
         x = sub ? t : d;
     }
-    const float rf = __ull2float_rn(r);
-    if (HRB_RCPN) rn = rcp_approx(rf);  // the next half-step divides by r
     // the quotient of x by S is >= 0; an estimate of -1 (x/S within |e| of
     // 0 from above) is clamped to 0, which is then exact
-    float xf;
-    if (HRB_DF && !FIRST) {
-        xf = (!THEN && df >= rf) ? df - rf : df;
-    } else {
-        xf = __ull2float_rn(x);
-    }
-    const uint32_t ke2 = (uint32_t)max(qfloor(xf, rcp), 0);
+    const uint32_t ke2 = (uint32_t)max(qfloor(__ull2float_rn(x), rcp), 0);
     const uint64_t y = madd64(x, ke2, nS);
-#if HRB_DF
-    df = __ull2float_rn(y);
-#endif
+    const float rf = __ull2float_rn(r);
     // 0 < r < S, proved in float by one product: (rf - Sf) rf < 0 exactly
     // when 0 < rf < Sf (rf = 0, rf >= Sf and an overflow to +inf all fail
     // it).  r == 0 -- the expansion exhausted, rare before the count limit --
@@ -197,16 +168,14 @@ __device__ __forceinline__ bool hs_commit(float Lf, uint32_t& cL, uint32_t cS, u
 
 // Undo hs_fast's in-place update (all arithmetic mod 2^64 is exact) and
 // redo the half-step with hardware division.
-__device__ __forceinline__ void hs_redo(uint64_t& L, uint64_t S, float& Lf, uint64_t& d, float& df, float& rn,
-                                        uint32_t& k, uint32_t k2, bool sub, bool then_body) {
+__device__ __forceinline__ void hs_redo(uint64_t& L, uint64_t S, float& Lf, uint64_t& d, uint32_t& k, uint32_t k2,
+                                        bool sub, bool then_body) {
     const uint64_t L_old = L + (uint64_t)k * S;
     const uint64_t d_old = d + (uint64_t)k2 * S + (sub ? L : 0);
     const ExactStep e = hs_exact(L_old, S, d_old, then_body);
     L = e.Lp;
     Lf = __ull2float_rn(e.Lp);
-    rn = rcp_approx(Lf);
     d = e.dn;
-    df = __ull2float_rn(e.dn);
     k = e.k;
 }
 
@@ -229,13 +198,13 @@ __device__ __forceinline__ void pair_step(Slot& s0, Slot& s1, bool act0, bool ac
     const uint32_t cS0 = THEN ? s0.cB : s0.cA, cS1 = THEN ? s1.cB : s1.cA;
     uint32_t k0, k1, q0, q1;
     bool b0, b1, u0, u1;
-    hs_fast<THEN, FIRST>(L0, S0, Lf0, Sf0, s0.d, s0.df, s0.rn, k0, q0, u0, b0);
-    hs_fast<THEN, FIRST>(L1, S1, Lf1, Sf1, s1.d, s1.df, s1.rn, k1, q1, u1, b1);
+    hs_fast<THEN, FIRST>(L0, S0, Lf0, Sf0, s0.d, k0, q0, u0, b0);
+    hs_fast<THEN, FIRST>(L1, S1, Lf1, Sf1, s1.d, k1, q1, u1, b1);
     b0 = b0 && act0;
     b1 = b1 && act1;
     if (__any_sync(0xffffffffu, b0 || b1)) {
-        if (b0) hs_redo(L0, S0, Lf0, s0.d, s0.df, s0.rn, k0, q0, u0, THEN);
-        if (b1) hs_redo(L1, S1, Lf1, s1.d, s1.df, s1.rn, k1, q1, u1, THEN);
+        if (b0) hs_redo(L0, S0, Lf0, s0.d, k0, q0, u0, THEN);
+        if (b1) hs_redo(L1, S1, Lf1, s1.d, k1, q1, u1, THEN);
     }
     f0 = hs_commit(Lf0, cL0, cS0, s0.M, k0);
     f1 = hs_commit(Lf1, cL1, cS1, s1.M, k1);
@@ -251,10 +220,8 @@ __device__ __forceinline__ bool fast_pair(Slot& s0, Slot& s1, bool act0, bool ac
                                           uint32_t& q0, uint32_t& q1, bool& u0, bool& u1, bool& b0, bool& b1) {
     uint64_t& L0 = THEN ? s0.A : s0.B;
     uint64_t& L1 = THEN ? s1.A : s1.B;
-    hs_fast<THEN>(L0, THEN ? s0.B : s0.A, THEN ? s0.Af : s0.Bf, THEN ? s0.Bf : s0.Af, s0.d, s0.df, s0.rn, k0, q0, u0,
-                  b0);
-    hs_fast<THEN>(L1, THEN ? s1.B : s1.A, THEN ? s1.Af : s1.Bf, THEN ? s1.Bf : s1.Af, s1.d, s1.df, s1.rn, k1, q1, u1,
-                  b1);
+    hs_fast<THEN>(L0, THEN ? s0.B : s0.A, THEN ? s0.Af : s0.Bf, THEN ? s0.Bf : s0.Af, s0.d, k0, q0, u0, b0);
+    hs_fast<THEN>(L1, THEN ? s1.B : s1.A, THEN ? s1.Af : s1.Bf, THEN ? s1.Bf : s1.Af, s1.d, k1, q1, u1, b1);
     b0 = b0 && act0;
     b1 = b1 && act1;
     return __any_sync(0xffffffffu, b0 || b1);
@@ -272,14 +239,12 @@ __device__ __forceinline__ bool exact_half(Slot& s, bool th) {
         s.A = e.Lp;
         s.Af = __ull2float_rn(e.Lp);
         s.d = e.dn;
-        s.df = __ull2float_rn(e.dn);
         return hs_commit(s.Af, s.cA, s.cB, s.M, e.k);
     }
     const ExactStep e = hs_exact(s.B, s.A, s.d, false);
     s.B = e.Lp;
     s.Bf = __ull2float_rn(e.Lp);
     s.d = e.dn;
-    s.df = __ull2float_rn(e.dn);
     return hs_commit(s.Bf, s.cB, s.cA, s.M, e.k);
 }
 
@@ -291,7 +256,7 @@ __device__ __noinline__ uint32_t slow_finish(Slot& s, bool bad, uint32_t k, uint
     uint64_t& L = th ? s.A : s.B;
     float& Lf = th ? s.Af : s.Bf;
     const uint64_t S = th ? s.B : s.A;
-    if (bad) hs_redo(L, S, Lf, s.d, s.df, s.rn, k, q, u, th);
+    if (bad) hs_redo(L, S, Lf, s.d, k, q, u, th);
     bool f = th ? hs_commit(s.Af, s.cA, s.cB, s.M, k) : hs_commit(s.Bf, s.cB, s.cA, s.M, k);
     h++;
     while (!f) {
@@ -325,10 +290,8 @@ __device__ __forceinline__ bool slot_init(uint64_t a, uint64_t b, uint64_t eps, 
     s.A = (W == 64) ? (0ull - a) : ((1ull << 32) - a);
     s.B = a;
     s.d = b;
-    s.df = __ull2float_rn(b);
     s.Af = __ull2float_rn(s.A);
     s.Bf = __ull2float_rn(a);
-    s.rn = rcp_approx(s.Bf);  // the first then-half divides by B = a
     s.cA = 1;
     s.cB = 1;
     s.M = N - 2;  // N >= 2 here
