@@ -167,7 +167,7 @@ __device__ __forceinline__ bool cslot_post(CSlot& s, float rf, uint32_t k, bool 
 struct ClQueue {  // the searches' initial states, structure of arrays
     uint64_t p[32 * HRB_CL_CHUNK], q[32 * HRB_CL_CHUNK], d[32 * HRB_CL_CHUNK], e[32 * HRB_CL_CHUNK];
     float pf[32 * HRB_CL_CHUNK], qf[32 * HRB_CL_CHUNK];
-    uint32_t M[32 * HRB_CL_CHUNK], tag[32 * HRB_CL_CHUNK];  // tag: owner lane | item << 8 | st << 16
+    uint32_t M[32 * HRB_CL_CHUNK], tag[32 * HRB_CL_CHUNK];  // tag: owner lane | item << 8 | flags << 16
     uint32_t fails[32];
 };
 
