@@ -661,19 +661,29 @@ __global__ void __launch_bounds__(256, HRB_P3_MINB) phase3_kernel(SliceDev s, in
             D1 += D2x32;
             const bool any = x0 < len && lo_top <= KtopM;
             if (__any_sync(0xffffffffu, any)) {
-                // rare: replay the proxy over the block; only the arguments it
-                // flags (the true hits, and near-misses within MARGIN of the
-                // window's top word) are evaluated exactly -- V(x) = V0 +
-                // x D1 + C(x,2) D2 -- and appended in argument order
-                uint32_t pu = (uint32_t)(V0 >> 96) + MARGIN, pd = (uint32_t)(D10 >> 96);
-                for (uint32_t x = 0; x < 32; x++) {
-                    const bool flag = any && x0 + x < len && pu <= KtopM;
-                    pu += pd;
-                    pd += e32;
-                    if (!__any_sync(0xffffffffu, flag)) continue;
+                // rare: replay the proxy over the block into a per-lane mask
+                // of the arguments it flags (the true hits, and near-misses
+                // within MARGIN of the window's top word; no votes), then
+                // evaluate exactly -- V(x) = V0 + x D1 + C(x,2) D2 -- one
+                // flagged argument per lane per round, lowest first, so each
+                // lane appends its hits in argument order
+                uint32_t fl = 0;
+                if (any) {
+                    uint32_t pu = (uint32_t)(V0 >> 96) + MARGIN, pd = (uint32_t)(D10 >> 96);
+#pragma unroll
+                    for (uint32_t x = 0; x < 32; x++) {
+                        fl |= (x0 + x < len && pu <= KtopM) ? (1u << x) : 0u;
+                        pu += pd;
+                        pd += e32;
+                    }
+                }
+                while (__any_sync(0xffffffffu, fl != 0)) {
                     bool hit = false;
                     u128 v = 0;
-                    if (flag) {
+                    uint32_t x = 0;
+                    if (fl) {
+                        x = (uint32_t)(__ffs(fl) - 1);
+                        fl &= fl - 1;
                         v = V0 + D10 * (u128)x + D2 * (u128)((x * (x - 1)) >> 1);
                         hit = v < K;
                     }
