@@ -577,6 +577,9 @@ __global__ void chunk3_kernel(unsigned long long* meta, const uint64_t* sub_coun
 #ifndef HRB_P3_MINB
 #define HRB_P3_MINB 3
 #endif
+#ifndef P3BLK
+#define P3BLK 64  // phase-3 proxy block: arguments per exact 128-bit advance
+#endif
 template <bool NARROW>
 __global__ void __launch_bounds__(256, HRB_P3_MINB) phase3_kernel(SliceDev s, int split, const uint64_t* sub_keys,
                                                      const uint32_t* sub_t, const uint64_t* sub_count,
@@ -636,13 +639,17 @@ __global__ void __launch_bounds__(256, HRB_P3_MINB) phase3_kernel(SliceDev s, in
         // either side).  Two instructions per argument; the exact 128-bit
         // state advances once per 32 arguments and a block is re-examined
         // only when some lane's proxy flagged it.
-        constexpr uint32_t MARGIN = 1024;
+        // blocks of P3BLK arguments (a power of two dividing CHUNK3); the
+        // proxy's floor error after x < P3BLK steps is at most x + C(x, 2)
+        constexpr uint32_t BLK = P3BLK, LBLK = BLK == 64 ? 6 : 5;
+        constexpr uint32_t MARGIN = BLK == 64 ? 4096 : 1024;
+        using Mask = typename std::conditional<BLK == 64, unsigned long long, uint32_t>::type;
         const uint32_t Ktop = (uint32_t)(K >> 96);
         const uint32_t KtopM = Ktop > 0xFFFFFFFFu - MARGIN ? 0xFFFFFFFFu : Ktop + MARGIN;
         const uint32_t e32 = (uint32_t)(D2 >> 96), e2x32 = 2 * e32;
-        const u128 D2x32 = D2 << 5, D2x496 = D2 * (u128)496;
+        const u128 D2xB = D2 << LBLK, D2xCB = D2 * (u128)(BLK * (BLK - 1) / 2);
         uint32_t rank = 0;
-        for (uint32_t x0 = 0; x0 < CHUNK3; x0 += 32) {
+        for (uint32_t x0 = 0; x0 < CHUNK3; x0 += BLK) {
             const u128 V0 = V, D10 = D1;
             uint32_t u = (uint32_t)(V >> 96) + MARGIN, d = (uint32_t)(D1 >> 96);
             uint32_t lo_top = 0xFFFFFFFFu;
@@ -651,14 +658,14 @@ __global__ void __launch_bounds__(256, HRB_P3_MINB) phase3_kernel(SliceDev s, in
             // (IADD3 -- an ALU-pipe op; two-input adds alone all went to the
             // FMA pipe as IMAD.IADD and throttled it); d(x+2) = d + 2e
 #pragma unroll
-            for (uint32_t x = 0; x < 32; x += 2) {
+            for (uint32_t x = 0; x < BLK; x += 2) {
                 const uint32_t t = u + d;
                 lo_top = min(lo_top, min(u, t));
                 u = t + d + e32;
                 d += e2x32;
             }
-            V += (D1 << 5) + D2x496;  // exact: 32 steps of V += D1, D1 += D2
-            D1 += D2x32;
+            V += (D1 << LBLK) + D2xCB;  // exact: BLK steps of V += D1, D1 += D2
+            D1 += D2xB;
             const bool any = x0 < len && lo_top <= KtopM;
             if (__any_sync(0xffffffffu, any)) {
                 // rare: replay the proxy over the block into a per-lane mask
@@ -667,12 +674,12 @@ __global__ void __launch_bounds__(256, HRB_P3_MINB) phase3_kernel(SliceDev s, in
                 // evaluate exactly -- V(x) = V0 + x D1 + C(x,2) D2 -- one
                 // flagged argument per lane per round, lowest first, so each
                 // lane appends its hits in argument order
-                uint32_t fl = 0;
+                Mask fl = 0;
                 if (any) {
                     uint32_t pu = (uint32_t)(V0 >> 96) + MARGIN, pd = (uint32_t)(D10 >> 96);
 #pragma unroll
-                    for (uint32_t x = 0; x < 32; x++) {
-                        fl |= (x0 + x < len && pu <= KtopM) ? (1u << x) : 0u;
+                    for (uint32_t x = 0; x < BLK; x++) {
+                        fl |= (x0 + x < len && pu <= KtopM) ? ((Mask)1 << x) : (Mask)0;
                         pu += pd;
                         pd += e32;
                     }
@@ -682,7 +689,7 @@ __global__ void __launch_bounds__(256, HRB_P3_MINB) phase3_kernel(SliceDev s, in
                     u128 v = 0;
                     uint32_t x = 0;
                     if (fl) {
-                        x = (uint32_t)(__ffs(fl) - 1);
+                        x = BLK == 64 ? (uint32_t)(__ffsll((long long)fl) - 1) : (uint32_t)(__ffs((int)fl) - 1);
                         fl &= fl - 1;
                         v = V0 + D10 * (u128)x + D2 * (u128)((x * (x - 1)) >> 1);
                         hit = v < K;
