@@ -27,6 +27,28 @@
 constexpr int WMAXD = 8;
 constexpr int WMAXNL = 8;
 
+// C(32, k), k <= 8 (all below 2^32)
+__host__ __device__ constexpr uint32_t wbinom32(int k) {
+    uint64_t b = 1;
+    for (int i = 0; i < k; i++) b = b * (uint64_t)(32 - i) / (uint64_t)(i + 1);
+    return (uint32_t)b;
+}
+
+// Bound on how far the 32-bit top-limb proxy of column 0 of a degree-D
+// difference table falls below the true top limb within 32 steps: each
+// column's proxy misses at most one carry per step and inherits the next
+// column's shortfall, e_l(x + 1) = e_l(x) + e_{l+1}(x) + 1, e_D = 0.
+template <int D>
+__host__ __device__ constexpr uint32_t wproxy_margin() {
+    uint64_t e[WMAXD + 1] = {};
+    uint64_t mx = 0;
+    for (int x = 0; x <= 32; x++) {
+        if (e[0] > mx) mx = e[0];
+        for (int l = 0; l < D; l++) e[l] = e[l] + e[l + 1] + 1;
+    }
+    return (uint32_t)(mx + 1);
+}
+
 struct WideDev {
     SliceDev g;  // geometry (S, n_dom, dom_n, last_n, dom_base, m0); coefficient fields unused
     int D, NL, ncoef;
@@ -570,16 +592,53 @@ __global__ void __launch_bounds__(128) phase3_wide_kernel(WideDev w, int split, 
 #pragma unroll
             for (int q = 0; q < NL; q++) K[q] = 0;
         }
+        // Hot loop, D <= 4, on 32-bit proxies of the columns' top limbs, each
+        // stepped by the next one's: a top limb misses at most one carry per
+        // step, so after x < 32 steps the proxy of column 0 lies below the
+        // true top limb by at most e(x) (wproxy_margin).  With u = proxy + M,
+        // V < K  =>  top(V) <= top(K)  =>  u <= top(K) + M (no wrap on either
+        // side).  D adds and half a min per argument instead of D NL-limb
+        // add-with-carry chains; the exact columns advance once per block of
+        // 32 (the closed form, sum of C(32, k) multiples), and a flagged block
+        // is re-walked exactly as before.  Higher degrees walk exactly: their
+        // margins (up to 1.5e7 at D = 8) would flag too many blocks.
+        constexpr bool PROXY = D <= 4;
+        constexpr uint32_t M = PROXY ? wproxy_margin<D>() : 0u;
         const uint32_t Ktop = K[NL - 1];
+        const uint32_t KtopM = Ktop > 0xFFFFFFFFu - M ? 0xFFFFFFFFu : Ktop + M;
         for (uint32_t xb = 0; xb < CHUNK3; xb += 32) {
             uint32_t lo_top = 0xFFFFFFFFu;  // conservative: V < K implies top limb(V) <= top limb(K)
-#pragma unroll 4
-            for (uint32_t x = 0; x < 32; x++) {
-                lo_top = min(lo_top, c[0][NL - 1]);
+            if constexpr (PROXY) {
+                uint32_t pr[D + 1];
 #pragma unroll
-                for (int l = 0; l < D; l++) addc_chain<NL>(c[l], c[l + 1]);
+                for (int l = 0; l <= D; l++) pr[l] = c[l][NL - 1];
+                pr[0] += M;
+#pragma unroll
+                for (uint32_t x = 0; x < 32; x++) {
+                    lo_top = min(lo_top, pr[0]);
+#pragma unroll
+                    for (int l = 0; l < D; l++) pr[l] += pr[l + 1];
+                }
+                // exact: c_l(x + 32) = sum_k C(32, k) c_{l+k}(x), in
+                // increasing l (each row reads only higher rows, not yet
+                // advanced)
+#pragma unroll
+                for (int l = 0; l < D; l++) {
+#pragma unroll
+                    for (int k = 1; l + k <= D; k++) {
+                        const uint32_t m1[1] = {wbinom32(k)};
+                        wmad<NL, 1>(c[l], c[l + k], m1);
+                    }
+                }
+            } else {
+#pragma unroll 4
+                for (uint32_t x = 0; x < 32; x++) {
+                    lo_top = min(lo_top, c[0][NL - 1]);
+#pragma unroll
+                    for (int l = 0; l < D; l++) addc_chain<NL>(c[l], c[l + 1]);
+                }
             }
-            const bool any = len > xb && lo_top <= Ktop;
+            const bool any = len > xb && lo_top <= KtopM;
             if (__any_sync(0xffffffffu, any)) {  // rare: re-walk the block exactly, append in order
                 uint32_t e[D + 1][NL];
                 if (len > xb) {
