@@ -535,7 +535,8 @@ def run_range(fn: str, binade: int, start: int, count: int, cfg: PipelineConfig,
     wide: a wide.WideGenConfig switches to the high-degree path (delta_R
     3..8, one Taylor model per large super-domain; the regular family; an
     extension of the reference, see wide.py) -- same records."""
-    from concurrent.futures import ThreadPoolExecutor
+    import contextlib
+    from concurrent.futures import Future, ThreadPoolExecutor
 
     from .shard import partition_blocks
     from .slices import pack_plan, plan_arrays
@@ -597,8 +598,12 @@ def run_range(fn: str, binade: int, start: int, count: int, cfg: PipelineConfig,
     records, stats_list, choices = [], [], []
     prev = None
     try:
-        with ThreadPoolExecutor(max_workers=1) as ex:
-            futs = {todo[0]: ex.submit(prepare, parts[todo[0]])} if todo else {}
+        # the first interval is prepared inline (nothing to overlap it with);
+        # a worker thread only exists when there is a next interval to prepare
+        # behind the current one (a thread's start and join cost milliseconds
+        # against a one-interval range's few)
+        with ThreadPoolExecutor(max_workers=1) if len(todo) > 1 else contextlib.nullcontext() as ex:
+            futs = {todo[0]: prepare(parts[todo[0]])} if todo else {}
             for k, part in enumerate(parts):
                 if k in done:  # restored from the manifest
                     bstart, algo, recs, st = done[k]
@@ -607,7 +612,9 @@ def run_range(fn: str, binade: int, start: int, count: int, cfg: PipelineConfig,
                     choices.append((bstart, algo))
                     prev = st
                     continue
-                batch = futs.pop(k).result()
+                batch = futs.pop(k)
+                if isinstance(batch, Future):
+                    batch = batch.result()
                 i = todo.index(k)
                 if i + 1 < len(todo):
                     futs[todo[i + 1]] = ex.submit(prepare, parts[todo[i + 1]])

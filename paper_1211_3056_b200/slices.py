@@ -485,26 +485,46 @@ def plan_arrays(fn: str, binade: int, fmt: FpFormat, pg: PolyGenConfig, start: i
         piece = Domain((1 << (fmt.precision - 1)) + lo, binade + 1, hi - lo, 0)
         n_p = piece_domain_size(fn, piece, e_out, fmt, pg.N)
         block = pg.tau * n_p
-        bst = lo + np.arange(0, -(-(hi - lo) // block), dtype=np.uint64) * np.uint64(block)
-        bcnt = np.minimum(np.uint64(block), np.uint64(hi) - bst)
-        full = (bcnt == np.uint64(block)) & (n_p == pg.N)
-        tau_t = (bcnt + np.uint64(n_p - 1)) // np.uint64(n_p)
-        tau = np.where(full, np.uint64(pg.tau), tau_t).astype(np.uint32)
+        # every block of a piece is full-sized but its last: constant columns
+        # with the last row patched (a block is "full" -- the tau/mu/nu
+        # schedule -- when it holds `block` arguments and n_p == N)
+        nb = -(-(hi - lo) // block)
+        last = hi - lo - (nb - 1) * block
+        tau_last = -(-last // n_p)
+        mid_full = n_p == pg.N
+        bst = np.arange(nb, dtype=np.uint64)
+        bst *= np.uint64(block)
+        bst += np.uint64(lo)
+        bcnt = np.full(nb, block, dtype=np.uint64)
+        bcnt[-1] = last
+        tau = np.full(nb, pg.tau, dtype=np.uint32)
+        tau[-1] = tau_last
+        mu = np.full(nb, pg.mu if mid_full else 1, dtype=np.uint32)
+        nu = np.full(nb, pg.nu, dtype=np.uint32) if mid_full else tau.copy()
+        if not (mid_full and last == block):
+            mu[-1], nu[-1] = 1, tau_last
+        ids = np.arange(nb, dtype=np.uint64)
+        ids *= np.uint64(pg.tau)
+        ids += np.uint64(next_id)
         cols["bstart"].append(bst)
         cols["bcount"].append(bcnt)
-        cols["n_p"].append(np.full(len(bst), n_p, dtype=np.uint32))
+        cols["n_p"].append(np.full(nb, n_p, dtype=np.uint32))
         cols["tau"].append(tau)
-        cols["mu"].append(np.where(full, pg.mu, 1).astype(np.uint32))
-        cols["nu"].append(np.where(full, pg.nu, tau).astype(np.uint32))
-        cols["e_out"].append(np.full(len(bst), e_out, dtype=np.int32))
-        ids = np.zeros(len(bst), dtype=np.uint64)
-        np.cumsum(tau[:-1].astype(np.uint64), out=ids[1:])
-        cols["dom_id0"].append(ids + np.uint64(next_id))
-        next_id += int(tau.astype(np.uint64).sum())
+        cols["mu"].append(mu)
+        cols["nu"].append(nu)
+        cols["e_out"].append(np.full(nb, e_out, dtype=np.int32))
+        cols["dom_id0"].append(ids)
+        next_id += pg.tau * (nb - 1) + tau_last
     dt = {"bstart": np.uint64, "bcount": np.uint64, "n_p": np.uint32, "tau": np.uint32, "mu": np.uint32,
           "nu": np.uint32, "e_out": np.int32, "dom_id0": np.uint64}
-    return BlockPlan(fn, binade, fmt, pg, *(np.concatenate(cols[k]).astype(dt[k]) if cols[k]
-                                            else np.zeros(0, dt[k]) for k in _PLAN_COLS))
+
+    def column(k):  # no copy for the usual one-piece range
+        c = cols[k]
+        if not c:
+            return np.zeros(0, dt[k])
+        return (c[0] if len(c) == 1 else np.concatenate(c)).astype(dt[k], copy=False)
+
+    return BlockPlan(fn, binade, fmt, pg, *(column(k) for k in _PLAN_COLS))
 
 
 def _signed_limbs(col: np.ndarray) -> int:
