@@ -94,6 +94,14 @@ def prepare_rank(args, rank, world, workers):
     return batch, time.perf_counter() - t0
 
 
+def gen_where(cfg, n_super: int) -> str:
+    """Where pack_plan generated the rank's packed blocks (its own choice)."""
+    from paper_1211_3056_b200.slices import _device_gen_ok
+
+    return ("on the device: hrb_pack_blocks" if _device_gen_ok(cfg.polygen, n_super) else
+            "on the host: libhrbhost.so") + ", bit-identical to mpmath"
+
+
 def generation_timing(args, rank, world, workers, prep_s):
     """The native generation of the rank's blocks (Taylor models, split,
     checks, packed columns) timed both ways after one warm call each: on the
@@ -607,8 +615,8 @@ def main():
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u64",
-            "data": f"synthetic: {args.fn} binade [1,2) argument ranges, Taylor blocks generated on the host "
-                    f"({'native, bit-identical to mpmath' if batch.supers.__class__.__name__ == 'PackedSupers' else 'mpmath'})",
+            "data": f"synthetic: {args.fn} binade [1,2) argument ranges, Taylor blocks generated "
+                    f"({gen_where(make_cfg(args), batch.n_super) if batch.supers.__class__.__name__ == 'PackedSupers' else 'on the host: mpmath'})",
             "config": {"workload": workload_name(args),
                        "parallelism": f"shard{world} (contiguous super-domain blocks, no collective on the hot path; "
                                       f"NCCL gather of counters + candidates at the end)",

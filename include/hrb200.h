@@ -207,6 +207,19 @@ int hrb_run_slice_host(const hrb_slice* host_slice, int algo, int mode, int spli
                        uint64_t cand_cap, float* device_ms);
 
 /*
+ * hrb_run_slice_host for a slice already resident in device memory (every
+ * column pointer a device pointer, e.g. hrb_pack_blocks' outputs plus the
+ * uploaded size columns): nothing is uploaded; the call's compute stream
+ * waits for the work already enqueued on `stream` (the generation), runs
+ * the three phases and copies counts[6] and the candidates to the HOST
+ * buffers, synchronised.  No failing-id list.  run_range's path when the
+ * generation ran on the device (funnel.execute_batch_host).
+ */
+int hrb_run_slice_resident(const hrb_slice* device_slice, int algo, int mode, int split,
+                           uint64_t* counts, uint64_t* cand_index, uint64_t* cand_dist,
+                           uint64_t* cand_dom, uint64_t cand_cap, float* device_ms, void* stream);
+
+/*
  * High-degree slices (delta_R = degree in 3..8): one Taylor polynomial per
  * large super-domain (up to 2^25 domains), the paper's large super-domain
  * generation.  The reference rejects delta >= 3

@@ -34,6 +34,7 @@ EXPORTS = (
     "hrb_phase3",
     "hrb_run_slice",
     "hrb_run_slice_host",
+    "hrb_run_slice_resident",
     "hrb_wrun_slice",
     "hrb_wrun_slice_host",
     "hrb_wdomain_coefficients",
@@ -123,6 +124,7 @@ def _declare(lib) -> None:
     lib.hrb_run_slice.argtypes = [C.POINTER(HrbSlice), I, I, I, C.POINTER(HrbRunOut), P]
     lib.hrb_run_slice_host.argtypes = [C.POINTER(HrbSlice), I, I, I, P, P, U64, P, P, P, U64,
                                        C.POINTER(C.c_float)]
+    lib.hrb_run_slice_resident.argtypes = [C.POINTER(HrbSlice), I, I, I, P, P, P, P, U64, C.POINTER(C.c_float), P]
     lib.hrb_wrun_slice.argtypes = [C.POINTER(HrbWSlice), I, I, C.POINTER(HrbRunOut), P]
     lib.hrb_wrun_slice_host.argtypes = [C.POINTER(HrbWSlice), I, I, P, P, P, P, U64, C.POINTER(C.c_float)]
     lib.hrb_wdomain_coefficients.argtypes = [C.POINTER(HrbWSlice), P, P]

@@ -1970,9 +1970,15 @@ HostRunState g_host[64];
 std::mutex g_host_mu[64];  // one host-buffer call at a time per device (shared buffers, streams)
 }  // namespace
 
-int hrb_run_slice_host(const hrb_slice* hs, int algo, int mode, int split, uint64_t* counts, uint64_t* fail_ids,
-                       uint64_t fail_cap, uint64_t* cand_index, uint64_t* cand_dist, uint64_t* cand_dom,
-                       uint64_t cand_cap, float* device_ms) {
+}  // extern "C"
+
+namespace {
+// hrb_run_slice_host and hrb_run_slice_resident: with `resident` the slice's
+// columns are already device pointers (written on stream `after`, e.g. by
+// hrb_pack_blocks) and nothing is uploaded.
+int run_host_impl(const hrb_slice* hs, bool resident, cudaStream_t after, int algo, int mode, int split,
+                  uint64_t* counts, uint64_t* fail_ids, uint64_t fail_cap, uint64_t* cand_index,
+                  uint64_t* cand_dist, uint64_t* cand_dom, uint64_t cand_cap, float* device_ms) {
     int rc = check_slice(hs);
     if (rc || (rc = check_algo(algo, mode))) return rc;
     int dev = 0;
@@ -1997,11 +2003,12 @@ int hrb_run_slice_host(const hrb_slice* hs, int algo, int mode, int split, uint6
     // limbs, only the low four of each coefficient are uploaded
     const int64_t CLd = CL >= 4 ? 4 : CL;
     const size_t b_coef = sizeof(uint32_t) * 6 * CLd * S, b2 = sizeof(uint64_t) * 2 * S, b32 = sizeof(uint32_t) * S;
-    if ((rc = H.coef.ensure(b_coef)) || (rc = H.G.ensure(b2)) || (rc = H.s2.ensure(b2)) || (rc = H.nd.ensure(b32)) ||
-        (rc = H.dn.ensure(b32)) || (rc = H.ln.ensure(b32)) || (rc = H.db.ensure(sizeof(uint64_t) * (S + 1))) ||
-        (rc = H.m0.ensure(sizeof(uint64_t) * S)) || (rc = H.counts.ensure(sizeof(uint64_t) * 6)) ||
-        (rc = H.ready.ensure(2 * sizeof(uint32_t))))
+    if (!resident &&
+        ((rc = H.coef.ensure(b_coef)) || (rc = H.G.ensure(b2)) || (rc = H.s2.ensure(b2)) || (rc = H.nd.ensure(b32)) ||
+         (rc = H.dn.ensure(b32)) || (rc = H.ln.ensure(b32)) || (rc = H.db.ensure(sizeof(uint64_t) * (S + 1))) ||
+         (rc = H.m0.ensure(sizeof(uint64_t) * S))))
         return rc;
+    if ((rc = H.counts.ensure(sizeof(uint64_t) * 6)) || (rc = H.ready.ensure(2 * sizeof(uint32_t)))) return rc;
     cudaStream_t st = H.st, cs = H.cs;
     // Upload on the copy stream.  The per-super-domain sizes and offsets go
     // first (prep and phase 1's tile walk need them before the launch).  For
@@ -2014,14 +2021,20 @@ int hrb_run_slice_host(const hrb_slice* hs, int algo, int mode, int split, uint6
     // run (cudaFree synchronises the device) must never wait on a kernel that
     // waits on a copy not yet issued.  The classic family (no wait in its
     // kernel) uploads everything before the search starts.
-    const bool stream_in = algo >= hrb::ALGO_REGULAR;
+    const bool stream_in = !resident && algo >= hrb::ALGO_REGULAR;
+    if (resident) {
+        CK(cudaEventRecord(H.edata, after));
+        CK(cudaStreamWaitEvent(st, H.edata, 0));
+    }
     CK(cudaEventRecord(H.e0, st));
     CK(cudaStreamWaitEvent(cs, H.e0, 0));  // nothing of the previous call still reads the buffers
     CK(cudaMemsetAsync(H.ready.p, 0, 2 * sizeof(uint32_t), cs));  // chunk counter, timeout flag
-    CK(cudaMemcpyAsync(H.nd.p, hs->n_dom, b32, cudaMemcpyHostToDevice, cs));
-    CK(cudaMemcpyAsync(H.dn.p, hs->dom_n, b32, cudaMemcpyHostToDevice, cs));
-    CK(cudaMemcpyAsync(H.ln.p, hs->last_n, b32, cudaMemcpyHostToDevice, cs));
-    CK(cudaMemcpyAsync(H.db.p, hs->dom_base, sizeof(uint64_t) * (S + 1), cudaMemcpyHostToDevice, cs));
+    if (!resident) {
+        CK(cudaMemcpyAsync(H.nd.p, hs->n_dom, b32, cudaMemcpyHostToDevice, cs));
+        CK(cudaMemcpyAsync(H.dn.p, hs->dom_n, b32, cudaMemcpyHostToDevice, cs));
+        CK(cudaMemcpyAsync(H.ln.p, hs->last_n, b32, cudaMemcpyHostToDevice, cs));
+        CK(cudaMemcpyAsync(H.db.p, hs->dom_base, sizeof(uint64_t) * (S + 1), cudaMemcpyHostToDevice, cs));
+    }
     const int64_t nchunk = !stream_in ? 1 : (S < UPLOAD_CHUNKS ? S : UPLOAD_CHUNKS);
     const int64_t per = (S + nchunk - 1) / nchunk;
     auto upload_chunk = [&](int64_t c) -> int {
@@ -2043,7 +2056,9 @@ int hrb_run_slice_host(const hrb_slice* hs, int algo, int mode, int split, uint6
             CK(cudaMemcpyAsync(H.ready.p, H.hseq + c, sizeof(uint32_t), cudaMemcpyHostToDevice, cs));
         return HRB_OK;
     };
-    if (!stream_in) {
+    if (resident) {
+        // the columns are on the device already
+    } else if (!stream_in) {
         if ((rc = upload_chunk(0))) return rc;
         CK(cudaEventRecord(H.edata, cs));
         CK(cudaStreamWaitEvent(st, H.edata, 0));
@@ -2059,15 +2074,17 @@ int hrb_run_slice_host(const hrb_slice* hs, int algo, int mode, int split, uint6
         up.chunk = (uint32_t)per;
     }
     hrb_slice ds = *hs;
-    ds.coef = (const uint32_t*)H.coef.p;
-    ds.coef_limbs = (int32_t)CLd;
-    ds.G = (const uint64_t*)H.G.p;
-    ds.s2abs = (const uint64_t*)H.s2.p;
-    ds.n_dom = (const uint32_t*)H.nd.p;
-    ds.dom_n = (const uint32_t*)H.dn.p;
-    ds.last_n = (const uint32_t*)H.ln.p;
-    ds.dom_base = (const uint64_t*)H.db.p;
-    ds.m0 = (const uint64_t*)H.m0.p;
+    if (!resident) {
+        ds.coef = (const uint32_t*)H.coef.p;
+        ds.coef_limbs = (int32_t)CLd;
+        ds.G = (const uint64_t*)H.G.p;
+        ds.s2abs = (const uint64_t*)H.s2.p;
+        ds.n_dom = (const uint32_t*)H.nd.p;
+        ds.dom_n = (const uint32_t*)H.dn.p;
+        ds.last_n = (const uint32_t*)H.ln.p;
+        ds.dom_base = (const uint64_t*)H.db.p;
+        ds.m0 = (const uint64_t*)H.m0.p;
+    }
     uint64_t sub_cap = (uint64_t)NT / 8 + 1024;  // grown once from the true count
     const uint64_t fcap = (uint64_t)NT;
     bool fail_copied = false;
@@ -2130,6 +2147,23 @@ int hrb_run_slice_host(const hrb_slice* hs, int algo, int mode, int split, uint6
     if (counts[0] > fail_cap && fail_ids) return set_err(HRB_ERR_CAPACITY, "fail_ids buffer too small");
     if (counts[2] > cand_cap) return set_err(HRB_ERR_CAPACITY, "candidate buffer too small");
     return HRB_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int hrb_run_slice_host(const hrb_slice* hs, int algo, int mode, int split, uint64_t* counts, uint64_t* fail_ids,
+                       uint64_t fail_cap, uint64_t* cand_index, uint64_t* cand_dist, uint64_t* cand_dom,
+                       uint64_t cand_cap, float* device_ms) {
+    return run_host_impl(hs, false, nullptr, algo, mode, split, counts, fail_ids, fail_cap, cand_index, cand_dist,
+                         cand_dom, cand_cap, device_ms);
+}
+
+int hrb_run_slice_resident(const hrb_slice* s, int algo, int mode, int split, uint64_t* counts,
+                           uint64_t* cand_index, uint64_t* cand_dist, uint64_t* cand_dom, uint64_t cand_cap,
+                           float* device_ms, void* stream) {
+    return run_host_impl(s, true, (cudaStream_t)stream, algo, mode, split, counts, nullptr, 0, cand_index, cand_dist,
+                         cand_dom, cand_cap, device_ms);
 }
 
 }  // extern "C"

@@ -274,6 +274,39 @@ def run_slice_host(batch: SliceBatch, algo_code: int, mode_code: int, split: int
     return HostSliceResult(counts, cm, cd, cdom, ms)
 
 
+def run_slice_resident(batch: SliceBatch, algo_code: int, mode_code: int, split: int,
+                       cand_cap: int = 1 << 16) -> HostSliceResult:
+    """run_slice_host for a batch whose generated columns are still on the
+    device (batch.resident, pack_plan's device generation inside run_range):
+    the size columns are uploaded, the columns are not -- one
+    hrb_run_slice_resident call on the current stream."""
+    torch = nat.require_cuda()
+    lib = nat.load()
+    r = batch.resident
+    u32 = lambda a: _t(torch, a.view(np.int32), r.device)  # noqa: E731
+    u64 = lambda a: _t(torch, a.view(np.int64), r.device)  # noqa: E731
+    keep = [u32(batch.n_dom), u32(batch.dom_n), u32(batch.last_n), u64(batch.dom_base), u64(batch.m0)]
+    desc = nat.HrbSlice(n_super=batch.n_super, n_total=batch.n_total, max_dom_n=batch.max_dom_n,
+                        coef_limbs=r.coef.shape[1], frac_bits=batch.frac_bits, word_bits=batch.word_bits,
+                        delta=batch.delta, coef=r.coef.data_ptr(), G=r.G.data_ptr(), s2abs=r.s2abs.data_ptr(),
+                        n_dom=keep[0].data_ptr(), dom_n=keep[1].data_ptr(), last_n=keep[2].data_ptr(),
+                        dom_base=keep[3].data_ptr(), m0=keep[4].data_ptr())
+    counts = np.zeros(6, dtype=np.uint64)
+    while True:
+        cm, cd, cdom = (np.zeros(max(cand_cap, 1), dtype=np.uint64) for _ in range(3))
+        ms = C.c_float(0)
+        rc = lib.hrb_run_slice_resident(C.byref(desc), algo_code, mode_code, split, counts.ctypes.data,
+                                        cm.ctypes.data, cd.ctypes.data, cdom.ctypes.data, cand_cap, C.byref(ms),
+                                        nat.stream_ptr())
+        if rc == nat.HRB_ERR_CAPACITY and counts[2] > cand_cap:
+            cand_cap = int(counts[2])
+            continue
+        nat.check("hrb_run_slice_resident", rc)
+        break
+    nc = int(counts[2])
+    return HostSliceResult(counts, cm[:nc], cd[:nc], cdom[:nc], ms.value)
+
+
 def domain_coefficients(ds: DeviceSlice) -> np.ndarray:
     """hrb_domain_coefficients -> uint32 [3, CL, n_total] (two's complement)."""
     torch = ds.torch
@@ -362,17 +395,42 @@ def search_verdict_arrays(algo_code: int, word_bits: int, a, b, eps, count, devi
 PIN_GEN_MIN = 8192  # super-domains from which pack_columns_device downloads into pinned memory
 
 
-def pack_columns_device(cfg, index_start, count, n_p, tau, e_out, device=None):
+class ResidentColumns:
+    """The device copies of a slice's generated columns (hrb_pack_blocks'
+    coef, G, s2abs) kept for hrb_run_slice_resident, while their download to
+    the host arrays of the same SliceBatch runs on a side stream: the host
+    arrays are valid only after wait()."""
+
+    def __init__(self, coef, G, s2abs, done, device):
+        self.coef, self.G, self.s2abs, self.done, self.device = coef, G, s2abs, done, device
+
+    def wait(self) -> None:
+        self.done.synchronize()
+
+    def upload(self, coef: np.ndarray, G: np.ndarray, s2abs: np.ndarray) -> None:
+        """Replace the device columns by the host ones (after host-side patches)."""
+        import torch
+
+        self.wait()
+        for d, h in ((self.coef, coef.view(np.int32)), (self.G, G.view(np.int64)), (self.s2abs, s2abs.view(np.int64))):
+            d.copy_(torch.from_numpy(np.ascontiguousarray(h)))
+
+
+def pack_columns_device(cfg, index_start, count, n_p, tau, e_out, device=None, resident: bool = False):
     """hrb_pack_blocks: the native generation (hostgen.pack_columns' Taylor
     models, split, checks and packed columns) with one device thread per
     super-domain, the same source as the host library.  Returns host numpy
-    arrays (coef, G, s2abs, status, shift_ok) like hostgen.pack_columns."""
+    arrays (coef, G, s2abs, status, shift_ok) like hostgen.pack_columns.
+    resident=True also returns a ResidentColumns (appended to the tuple):
+    the columns stay on the device for the search and their download runs
+    behind it -- the returned coef / G / s2abs arrays are filled only once
+    its wait() returned (status and shift_ok are final on return)."""
     torch = nat.require_cuda()
     lib = nat.load()
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
     if dev.index is not None and dev.index != torch.cuda.current_device():
         with torch.cuda.device(dev):  # the library launches on the current device's stream
-            return pack_columns_device(cfg, index_start, count, n_p, tau, e_out, dev)
+            return pack_columns_device(cfg, index_start, count, n_p, tau, e_out, dev, resident)
     S = len(index_start)
     cl = cfg.limbs + 1
 
@@ -394,12 +452,28 @@ def pack_columns_device(cfg, index_start, count, n_p, tau, e_out, device=None):
     # it has to fault in fresh pages, and the pinned columns also make the
     # later upload of the slice a direct DMA
     # (small slices: pageable; pinning fresh host memory costs more than it saves)
-    pin = S >= PIN_GEN_MIN
-    outs = []
-    for t in (coef, G, s2, status, ok2):
-        h = torch.empty(t.shape, dtype=t.dtype, pin_memory=pin)
-        h.copy_(t, non_blocking=pin)
-        outs.append(h)
-    torch.cuda.current_stream(dev).synchronize()
-    return (outs[0].numpy().view(np.uint32), outs[1].numpy().view(np.uint64), outs[2].numpy().view(np.uint64),
+    pin = S >= PIN_GEN_MIN or resident
+    cur = torch.cuda.current_stream(dev)
+    outs = [torch.empty(t.shape, dtype=t.dtype, pin_memory=pin) for t in (coef, G, s2, status, ok2)]
+    res = None
+    if resident:
+        # the flags now (the caller decides on them), the columns behind the
+        # search on a side stream
+        outs[3].copy_(status, non_blocking=True)
+        outs[4].copy_(ok2, non_blocking=True)
+        flags = cur.record_event()
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(cur)
+        with torch.cuda.stream(side):
+            for h, t in zip(outs[:3], (coef, G, s2)):
+                h.copy_(t, non_blocking=True)
+                t.record_stream(side)
+        res = ResidentColumns(coef, G, s2, side.record_event(), dev)
+        flags.synchronize()
+    else:
+        for h, t in zip(outs, (coef, G, s2, status, ok2)):
+            h.copy_(t, non_blocking=pin)
+        cur.synchronize()
+    cols = (outs[0].numpy().view(np.uint32), outs[1].numpy().view(np.uint64), outs[2].numpy().view(np.uint64),
             outs[3].numpy(), outs[4].numpy())
+    return cols + (res,) if resident else cols

@@ -210,10 +210,20 @@ def execute_batch_host(batch: SliceBatch, cfg: PipelineConfig, algo: str, fn: st
     the statistics (counts and arguments covered per phase) come from the
     device.  The phase-1 row's wall_ms is the device time of all three
     phases (the call does not split it)."""
-    from .device import run_slice_host
+    from .device import run_slice_host, run_slice_resident
 
     fmt = cfg.fmt
-    res = run_slice_host(batch, ALGO_CODE[Algorithm(algo)], MODE_CODE[cfg.phase.div_mode], cfg.phase.phase2_split)
+    args = (batch, ALGO_CODE[Algorithm(algo)], MODE_CODE[cfg.phase.div_mode], cfg.phase.phase2_split)
+    if batch.resident is not None:
+        # generated on the device (pack_plan(resident=True)): search the
+        # columns where they are; their host copies land meanwhile
+        try:
+            res = run_slice_resident(*args)
+        finally:
+            batch.resident.wait()
+            batch.resident = None
+    else:
+        res = run_slice_host(*args)
     n_fail, n_sub, n_cand, iters, a2, a3 = (int(x) for x in res.counts)
     if batch.shift_bound_ok is not None and not batch.shift_bound_ok.all():
         # the MPInt replay needs the failing ids: rare (narrow limb budgets)
@@ -568,7 +578,8 @@ def run_range(fn: str, binade: int, start: int, count: int, cfg: PipelineConfig,
             torch.cuda.set_device(dev)
         if wide is not None:
             return pack_wide(plan[part[0]:part[1]], wide, w)
-        return pack_plan(plan[part[0]:part[1]], cfg.word_bits, budget_ceiling=ceiling, workers=w, native=native)
+        return pack_plan(plan[part[0]:part[1]], cfg.word_bits, budget_ceiling=ceiling, workers=w, native=native,
+                         resident=True)
 
     done, sink = {}, None
     if manifest is not None:

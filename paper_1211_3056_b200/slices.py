@@ -285,6 +285,9 @@ class SliceBatch:
     shift_bound_ok: np.ndarray = field(default=None)  # bool [S]
     counts: np.ndarray = field(default=None)  # uint64 [S] arguments per super-domain
     nus: np.ndarray = field(default=None)     # uint32 [S] packet length nu (the reference's packet walk)
+    # device copies of coef / G / s2abs still being downloaded into the
+    # arrays above (pack_plan(resident=True)); None once they are final
+    resident: object = field(default=None, repr=False, compare=False)
 
     def __post_init__(self) -> None:
         if self.counts is None:
@@ -579,7 +582,8 @@ def _device_gen_ok(pg: PolyGenConfig, n: int) -> bool:
 
 
 def pack_plan(plan: BlockPlan, word_bits: int, budget_ceiling: Fraction | None = None,
-              workers: int = 1, native: bool | None = None, device: bool | None = None) -> SliceBatch:
+              workers: int = 1, native: bool | None = None, device: bool | None = None,
+              resident: bool = False) -> SliceBatch:
     """Taylor models + split + checks + packing of planned blocks.
 
     With the native generation (exp on binades <= 0, delta <= 2, no budget
@@ -590,7 +594,11 @@ def pack_plan(plan: BlockPlan, word_bits: int, budget_ceiling: Fraction | None =
     threads.  Blocks it flags go through the exact Python path one by one
     (raising the reference's error where the reference raises).
     native=False forces the Python path; otherwise the native path runs
-    wherever it covers the configuration."""
+    wherever it covers the configuration.  resident=True (run_range): with
+    the device generation the columns also stay on the device
+    (batch.resident, device.ResidentColumns) and the host copies of coef /
+    G / s2abs are filled behind the search -- valid after
+    batch.resident.wait(), which funnel.execute_batch_host calls."""
     from . import hostgen
 
     fmt, pg = plan.fmt, plan.pg
@@ -607,22 +615,34 @@ def pack_plan(plan: BlockPlan, word_bits: int, budget_ceiling: Fraction | None =
     cfg = hostgen.make_cfg(plan.fn, fmt, pg, plan.binade, word_bits)
     if device is None:
         device = _device_gen_ok(pg, len(plan))
+    res = None
     if device:
         from .device import pack_columns_device
 
-        coef, G, s2, status, ok2 = pack_columns_device(cfg, plan.bstart, plan.bcount, plan.n_p, plan.tau, plan.e_out)
+        if resident:
+            coef, G, s2, status, ok2, res = pack_columns_device(cfg, plan.bstart, plan.bcount, plan.n_p, plan.tau,
+                                                                plan.e_out, resident=True)
+        else:
+            coef, G, s2, status, ok2 = pack_columns_device(cfg, plan.bstart, plan.bcount, plan.n_p, plan.tau,
+                                                           plan.e_out)
     else:
         coef, G, s2, status, ok2 = hostgen.pack_columns(cfg, plan.bstart, plan.bcount, plan.n_p, plan.tau,
                                                         plan.e_out, workers)
-    for t in np.flatnonzero(status != hostgen.HRBH_OK).tolist():
+    fallback = np.flatnonzero(status != hostgen.HRBH_OK).tolist()
+    if fallback and res is not None:
+        res.wait()  # the host columns are patched below, then sent back
+    for t in fallback:
         sd = _make_super(plan.block(t))  # exact Python path; raises where the reference raises
         c1, g1, s21, _, k1 = _pack_rows([sd], fmt, pg, word_bits, budget_ceiling, True)
         coef[:, :, t], G[:, t], s2[:, t], ok2[t] = c1[:, :, 0], g1[:, 0], s21[:, 0], k1[0]
+    if fallback and res is not None:
+        res.upload(coef, G, s2)
     n_dom = plan.tau.copy()
     dom_n = plan.n_p.copy()
     last_n = (plan.bcount - (plan.tau.astype(np.uint64) - np.uint64(1)) * plan.n_p.astype(np.uint64)).astype(np.uint32)
     dom_base = np.zeros(len(plan) + 1, dtype=np.uint64)
-    np.cumsum(n_dom, out=dom_base[1:])
+    np.cumsum(n_dom.astype(np.int64), out=dom_base[1:].view(np.int64))  # numpy's int64 scan is ~3x its uint64 one
     return SliceBatch(PackedSupers(plan, coef, pg.delta), fmt, plan.binade, F, word_bits, pg.delta, pg.limbs, coef,
                       G, s2, n_dom, dom_n, last_n, dom_base, plan.bstart.copy(), id0=int(plan.dom_id0[0]),
-                      shift_bound_ok=ok2.astype(bool), counts=plan.bcount.copy(), nus=plan.nu.copy())
+                      shift_bound_ok=ok2.astype(bool), counts=plan.bcount.copy(), nus=plan.nu.copy(),
+                      resident=res)

@@ -110,3 +110,65 @@ def test_pack_plan_device_raises_like_host(seed):
         for k in PACKED:
             assert np.array_equal(getattr(got, k), getattr(want, k)), k
         assert np.array_equal(got.shift_bound_ok, want.shift_bound_ok)
+
+
+@pytest.mark.parametrize("seed,flag_every", [(0, 0), (2, 7), (5, 0), (11, 3), (22, 0), (27, 1)])
+def test_pack_plan_resident_columns(seed, flag_every, monkeypatch):
+    """pack_plan(resident=True): the device columns it keeps for the search
+    equal the host slice, and the host copies landing behind it equal the
+    plain pack once waited for.  flag_every > 0 marks every k-th block as a
+    fallback (and zeroes its device columns): the exact Python path redoes
+    those rows and the patched columns must reach the device too."""
+    from paper_1211_3056_b200 import device as devmod
+
+    rng = random.Random(7000 + seed)
+    plan, fmt, pg, binade, W = _random_plan(rng)
+    want = slices.pack_plan(plan, W, workers=1, native=True, device=False)
+    if flag_every:
+        real = devmod.pack_columns_device
+
+        def flagged(*a, **k):
+            out = real(*a, **k)
+            status, res = out[3], out[5]
+            status[::flag_every] = hostgen.HRBH_FALLBACK
+            res.coef[:, :, ::flag_every] = 0
+            res.G[:, ::flag_every] = 0
+            res.s2abs[:, ::flag_every] = 0
+            return out
+
+        monkeypatch.setattr(devmod, "pack_columns_device", flagged)
+    got = slices.pack_plan(plan, W, workers=1, native=True, device=True, resident=True)
+    r = got.resident
+    assert r is not None
+    r.wait()
+    for k in PACKED:
+        assert np.array_equal(getattr(got, k), getattr(want, k)), k
+    assert np.array_equal(r.coef.cpu().numpy().view(np.uint32), want.coef)
+    assert np.array_equal(r.G.cpu().numpy().view(np.uint64), want.G)
+    assert np.array_equal(r.s2abs.cpu().numpy().view(np.uint64), want.s2abs)
+
+
+@pytest.mark.parametrize("eps_bits,log2_count", [(32, 30), (14, 24), (20, 27)])
+def test_resident_run_equals_host_buffer_run(eps_bits, log2_count):
+    """hrb_run_slice_resident on the generated device columns (run_range's
+    path) == hrb_run_slice_host on the host slice: counts (phases' outputs and
+    arguments covered), candidates, records."""
+    from paper_1211_3056_b200 import FpFormat, PhaseConfig, PipelineConfig
+    from paper_1211_3056_b200.funnel import execute_batch_host
+
+    N = 1 << 12
+    pg = PolyGenConfig(tau=64, N=N, mu=8, nu=8, delta=2, limbs=8, frac_bits=96, guard=32)
+    cfg = PipelineConfig("exp", FpFormat(53, eps_bits), pg, PhaseConfig("regular", phase2_split=8, N1=N))
+    plan = slices.plan_arrays("exp", 0, cfg.fmt, pg, 12345 << 20, 1 << log2_count)
+    host = slices.pack_plan(plan, 64, workers=2, device=False)
+    res = slices.pack_plan(plan, 64, workers=2, device=True, resident=True)
+    a = execute_batch_host(host, cfg, "regular", workers=2)
+    b = execute_batch_host(res, cfg, "regular", workers=2)
+    assert res.resident is None
+    assert a.records == b.records
+    assert a.iterations == b.iterations
+    assert [(r.phase, r.domains_in, r.domains_out, r.arguments_covered) for r in a.stats.rows] == \
+           [(r.phase, r.domains_in, r.domains_out, r.arguments_covered) for r in b.stats.rows]
+    assert a.candidates == b.candidates and len(a.candidates) > 0
+    for k in PACKED:
+        assert np.array_equal(getattr(res, k), getattr(host, k)), k
