@@ -283,9 +283,9 @@ def run_slice_resident(batch: SliceBatch, algo_code: int, mode_code: int, split:
     torch = nat.require_cuda()
     lib = nat.load()
     r = batch.resident
-    u32 = lambda a: _t(torch, a.view(np.int32), r.device)  # noqa: E731
-    u64 = lambda a: _t(torch, a.view(np.int64), r.device)  # noqa: E731
-    keep = [u32(batch.n_dom), u32(batch.dom_n), u32(batch.last_n), u64(batch.dom_base), u64(batch.m0)]
+    # the size columns: uploaded by pack_plan while the generation ran, else now
+    keep = r.extra if r.extra is not None else upload_columns(
+        torch, [batch.n_dom, batch.dom_n, batch.last_n, batch.dom_base, batch.m0], r.device)
     desc = nat.HrbSlice(n_super=batch.n_super, n_total=batch.n_total, max_dom_n=batch.max_dom_n,
                         coef_limbs=r.coef.shape[1], frac_bits=batch.frac_bits, word_bits=batch.word_bits,
                         delta=batch.delta, coef=r.coef.data_ptr(), G=r.G.data_ptr(), s2abs=r.s2abs.data_ptr(),
@@ -401,8 +401,9 @@ class ResidentColumns:
     the host arrays of the same SliceBatch runs on a side stream: the host
     arrays are valid only after wait()."""
 
-    def __init__(self, coef, G, s2abs, done, device):
+    def __init__(self, coef, G, s2abs, done, device, extra=None):
         self.coef, self.G, self.s2abs, self.done, self.device = coef, G, s2abs, done, device
+        self.extra = extra  # device copies of the caller's `during` columns (pack_columns_device)
 
     def wait(self) -> None:
         self.done.synchronize()
@@ -416,7 +417,26 @@ class ResidentColumns:
             d.copy_(torch.from_numpy(np.ascontiguousarray(h)))
 
 
-def pack_columns_device(cfg, index_start, count, n_p, tau, e_out, device=None, resident: bool = False):
+def upload_columns(torch, arrays, dev, pin: bool = True) -> list:
+    """Host 1-D columns -> device tensors of the same dtypes through ONE copy
+    (a staging buffer, page-locked when pin; 8-byte aligned segments):
+    each small pageable copy costs tens of microseconds on its own."""
+    arrays = [np.ascontiguousarray(a) for a in arrays]
+    offs, n = [], 0
+    for a in arrays:
+        offs.append(n)
+        n += -(-a.nbytes // 8) * 8
+    host = torch.empty(max(n, 8), dtype=torch.uint8, pin_memory=pin)
+    h = host.numpy()
+    for a, o in zip(arrays, offs):
+        h[o:o + a.nbytes] = a.view(np.uint8).reshape(-1)
+    dbuf = host.to(dev, non_blocking=pin)
+    tdt = {1: torch.uint8, 4: torch.int32, 8: torch.int64}
+    return [dbuf[o:o + a.nbytes].view(tdt[a.dtype.itemsize]) for a, o in zip(arrays, offs)]
+
+
+def pack_columns_device(cfg, index_start, count, n_p, tau, e_out, device=None, resident: bool = False,
+                        during=None):
     """hrb_pack_blocks: the native generation (hostgen.pack_columns' Taylor
     models, split, checks and packed columns) with one device thread per
     super-domain, the same source as the host library.  Returns host numpy
@@ -424,26 +444,29 @@ def pack_columns_device(cfg, index_start, count, n_p, tau, e_out, device=None, r
     resident=True also returns a ResidentColumns (appended to the tuple):
     the columns stay on the device for the search and their download runs
     behind it -- the returned coef / G / s2abs arrays are filled only once
-    its wait() returned (status and shift_ok are final on return)."""
+    its wait() returned (status and shift_ok are final on return).
+    during (resident only): a callable run on the host while the kernel
+    runs; the 1-D columns it returns are uploaded (one copy) and kept as
+    ResidentColumns.extra."""
     torch = nat.require_cuda()
     lib = nat.load()
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
     if dev.index is not None and dev.index != torch.cuda.current_device():
         with torch.cuda.device(dev):  # the library launches on the current device's stream
-            return pack_columns_device(cfg, index_start, count, n_p, tau, e_out, dev, resident)
+            return pack_columns_device(cfg, index_start, count, n_p, tau, e_out, dev, resident, during)
     S = len(index_start)
     cl = cfg.limbs + 1
 
-    def up(a, dt, view):
-        return torch.from_numpy(np.ascontiguousarray(a, dtype=dt).view(view)).to(dev, non_blocking=False)
-
-    ins = [up(index_start, np.uint64, np.int64), up(count, np.uint64, np.int64), up(n_p, np.uint32, np.int32),
-           up(tau, np.uint32, np.int32), up(e_out, np.int32, np.int32)]
-    coef = torch.zeros((6, cl, S), dtype=torch.int32, device=dev)
-    G = torch.zeros((2, S), dtype=torch.int64, device=dev)
-    s2 = torch.zeros((2, S), dtype=torch.int64, device=dev)
-    status = torch.zeros(S, dtype=torch.uint8, device=dev)
-    ok2 = torch.zeros(S, dtype=torch.uint8, device=dev)
+    pin = S >= PIN_GEN_MIN or resident
+    ins = upload_columns(torch, [np.asarray(index_start, dtype=np.uint64), np.asarray(count, dtype=np.uint64),
+                                 np.asarray(n_p, dtype=np.uint32), np.asarray(tau, dtype=np.uint32),
+                                 np.asarray(e_out, dtype=np.int32)], dev, pin)
+    # every column of every block is written (status decides which are valid)
+    coef = torch.empty((6, cl, S), dtype=torch.int32, device=dev)
+    G = torch.empty((2, S), dtype=torch.int64, device=dev)
+    s2 = torch.empty((2, S), dtype=torch.int64, device=dev)
+    status = torch.empty(S, dtype=torch.uint8, device=dev)
+    ok2 = torch.empty(S, dtype=torch.uint8, device=dev)
     nat.check("hrb_pack_blocks", lib.hrb_pack_blocks(C.byref(cfg), S, *(t.data_ptr() for t in ins), coef.data_ptr(),
                                                      G.data_ptr(), s2.data_ptr(), status.data_ptr(), ok2.data_ptr(),
                                                      nat.stream_ptr()))
@@ -452,7 +475,6 @@ def pack_columns_device(cfg, index_start, count, n_p, tau, e_out, device=None, r
     # it has to fault in fresh pages, and the pinned columns also make the
     # later upload of the slice a direct DMA
     # (small slices: pageable; pinning fresh host memory costs more than it saves)
-    pin = S >= PIN_GEN_MIN or resident
     cur = torch.cuda.current_stream(dev)
     outs = [torch.empty(t.shape, dtype=t.dtype, pin_memory=pin) for t in (coef, G, s2, status, ok2)]
     res = None
@@ -468,7 +490,8 @@ def pack_columns_device(cfg, index_start, count, n_p, tau, e_out, device=None, r
             for h, t in zip(outs[:3], (coef, G, s2)):
                 h.copy_(t, non_blocking=True)
                 t.record_stream(side)
-        res = ResidentColumns(coef, G, s2, side.record_event(), dev)
+        extra = upload_columns(torch, during(), dev) if during is not None else None
+        res = ResidentColumns(coef, G, s2, side.record_event(), dev, extra)
         flags.synchronize()
     else:
         for h, t in zip(outs, (coef, G, s2, status, ok2)):

@@ -615,13 +615,25 @@ def pack_plan(plan: BlockPlan, word_bits: int, budget_ceiling: Fraction | None =
     cfg = hostgen.make_cfg(plan.fn, fmt, pg, plan.binade, word_bits)
     if device is None:
         device = _device_gen_ok(pg, len(plan))
+    sizes = []
+
+    def size_columns():  # n_dom, dom_n, last_n, dom_base, m0
+        n_dom = plan.tau.copy()
+        last_n = (plan.bcount - (plan.tau.astype(np.uint64) - np.uint64(1)) * plan.n_p.astype(np.uint64)).astype(
+            np.uint32)
+        dom_base = np.zeros(len(plan) + 1, dtype=np.uint64)
+        np.cumsum(n_dom.astype(np.int64), out=dom_base[1:].view(np.int64))  # numpy's int64 scan: ~3x its uint64 one
+        sizes[:] = [n_dom, plan.n_p.copy(), last_n, dom_base, plan.bstart.copy()]
+        return sizes
+
     res = None
     if device:
         from .device import pack_columns_device
 
         if resident:
+            # the size columns are computed and uploaded while the kernel runs
             coef, G, s2, status, ok2, res = pack_columns_device(cfg, plan.bstart, plan.bcount, plan.n_p, plan.tau,
-                                                                plan.e_out, resident=True)
+                                                                plan.e_out, resident=True, during=size_columns)
         else:
             coef, G, s2, status, ok2 = pack_columns_device(cfg, plan.bstart, plan.bcount, plan.n_p, plan.tau,
                                                            plan.e_out)
@@ -637,12 +649,8 @@ def pack_plan(plan: BlockPlan, word_bits: int, budget_ceiling: Fraction | None =
         coef[:, :, t], G[:, t], s2[:, t], ok2[t] = c1[:, :, 0], g1[:, 0], s21[:, 0], k1[0]
     if fallback and res is not None:
         res.upload(coef, G, s2)
-    n_dom = plan.tau.copy()
-    dom_n = plan.n_p.copy()
-    last_n = (plan.bcount - (plan.tau.astype(np.uint64) - np.uint64(1)) * plan.n_p.astype(np.uint64)).astype(np.uint32)
-    dom_base = np.zeros(len(plan) + 1, dtype=np.uint64)
-    np.cumsum(n_dom.astype(np.int64), out=dom_base[1:].view(np.int64))  # numpy's int64 scan is ~3x its uint64 one
+    n_dom, dom_n, last_n, dom_base, m0 = sizes or size_columns()
     return SliceBatch(PackedSupers(plan, coef, pg.delta), fmt, plan.binade, F, word_bits, pg.delta, pg.limbs, coef,
-                      G, s2, n_dom, dom_n, last_n, dom_base, plan.bstart.copy(), id0=int(plan.dom_id0[0]),
+                      G, s2, n_dom, dom_n, last_n, dom_base, m0, id0=int(plan.dom_id0[0]),
                       shift_bound_ok=ok2.astype(bool), counts=plan.bcount.copy(), nus=plan.nu.copy(),
                       resident=res)
