@@ -13,7 +13,7 @@ for tool in memcheck racecheck synccheck; do
   # modes, and the device generation
   timeout 1500 compute-sanitizer --tool $tool --error-exitcode 9 --print-limit 20 \
      python -m pytest tests/test_gpu_parity.py tests/test_devgen_gpu.py -q -x \
-     -k "(iteration_sums and lefevre) or device_pack_equals_reference_fixture" > gpurun_out/sanitize2_$tool.log 2>&1
+     -k "(iteration_sums and lefevre) or device_pack_equals_reference_fixture or resident" > gpurun_out/sanitize2_$tool.log 2>&1
   echo "$tool rc=$?" >> gpurun_out/sanitize2_$tool.log
   tail -n 4 gpurun_out/sanitize2_$tool.log
 done
