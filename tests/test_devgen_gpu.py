@@ -172,3 +172,25 @@ def test_resident_run_equals_host_buffer_run(eps_bits, log2_count):
     assert a.candidates == b.candidates and len(a.candidates) > 0
     for k in PACKED:
         assert np.array_equal(getattr(res, k), getattr(host, k)), k
+
+
+def test_run_range_resident_intervals_equal_host_generation():
+    """run_range over 4 intervals with the device generation (each interval
+    prepared in the worker thread behind the previous one's search, searched
+    in place) == one host-generated, host-buffer slice of the whole range."""
+    from paper_1211_3056_b200 import FpFormat, PhaseConfig, PipelineConfig
+    from paper_1211_3056_b200.funnel import execute_batch_host, run_range
+
+    N = 1 << 12
+    pg = PolyGenConfig(tau=64, N=N, mu=8, nu=8, delta=2, limbs=8, frac_bits=96, guard=32)
+    cfg = PipelineConfig("exp", FpFormat(53, 20), pg, PhaseConfig("regular", phase2_split=8, N1=N))
+    start, count = 777 << 30, 1 << 33
+    plan = slices.plan_arrays("exp", 0, cfg.fmt, pg, start, count)
+    assert len(plan) // 4 >= slices.DEVICE_GEN_MIN
+    whole = execute_batch_host(slices.pack_plan(plan, 64, workers=2, device=False), cfg, "regular", workers=2)
+    out = run_range("exp", 0, start, count, cfg, interval_args=count // 4, workers=2)
+    assert len(out.interval_stats) == 4
+    assert out.records == whole.records and len(whole.records) > 0
+    for k in range(3):  # phases' domains out and arguments covered add up
+        assert sum(st.rows[k].domains_out for st in out.interval_stats) == whole.stats.rows[k].domains_out
+        assert sum(st.rows[k].arguments_covered for st in out.interval_stats) == whole.stats.rows[k].arguments_covered
