@@ -214,13 +214,17 @@ def execute_batch_host(batch: SliceBatch, cfg: PipelineConfig, algo: str, fn: st
 
     fmt = cfg.fmt
     args = (batch, ALGO_CODE[Algorithm(algo)], MODE_CODE[cfg.phase.div_mode], cfg.phase.phase2_split)
-    if batch.resident is not None:
+    r = batch.resident
+    if r is not None and r.device.index != _current_cuda_device():
+        r.wait()  # generated on another device: the host-buffer path below
+        batch.resident = r = None
+    if r is not None:
         # generated on the device (pack_plan(resident=True)): search the
         # columns where they are; their host copies land meanwhile
         try:
             res = run_slice_resident(*args)
         finally:
-            batch.resident.wait()
+            r.wait()
             batch.resident = None
     else:
         res = run_slice_host(*args)
