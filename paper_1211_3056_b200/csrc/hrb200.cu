@@ -657,12 +657,28 @@ __global__ void __launch_bounds__(256, HRB_P3_MINB) phase3_kernel(SliceDev s, in
             // a three-input min; u(x+2) = t + d + e as one three-input add
             // (IADD3 -- an ALU-pipe op; two-input adds alone all went to the
             // FMA pipe as IMAD.IADD and throttled it); d(x+2) = d + 2e
+#ifndef HRB_P3_ASM
+#define HRB_P3_ASM 1
+#endif
 #pragma unroll
             for (uint32_t x = 0; x < BLK; x += 2) {
+#if HRB_P3_ASM
+                // as opaque adds: the front end otherwise re-associates the
+                // chain into one add per argument for u and one for d (all
+                // IMAD.IADD, FMA pipe) and, seeing the replay below compute
+                // the same values, keeps them in local memory for it
+                uint32_t t;
+                asm("add.u32 %0, %1, %2;" : "=r"(t) : "r"(u), "r"(d));
+                lo_top = min(lo_top, min(u, t));
+                asm("{\n\t.reg .u32 w;\n\tadd.u32 w, %1, %2;\n\tadd.u32 %0, w, %3;\n\t}"
+                    : "=r"(u) : "r"(t), "r"(d), "r"(e32));
+                asm("add.u32 %0, %0, %1;" : "+r"(d) : "r"(e2x32));
+#else
                 const uint32_t t = u + d;
                 lo_top = min(lo_top, min(u, t));
                 u = t + d + e32;
                 d += e2x32;
+#endif
             }
             V += (D1 << LBLK) + D2xCB;  // exact: BLK steps of V += D1, D1 += D2
             D1 += D2xB;
