@@ -652,7 +652,13 @@ __global__ void __launch_bounds__(256, HRB_P3_MINB) phase3_kernel(SliceDev s, in
         for (uint32_t x0 = 0; x0 < CHUNK3; x0 += BLK) {
             const u128 V0 = V, D10 = D1;
             uint32_t u = (uint32_t)(V >> 96) + MARGIN, d = (uint32_t)(D1 >> 96);
-            uint32_t lo_top = 0xFFFFFFFFu;
+#ifndef HRB_P3_Q
+#define HRB_P3_Q 4  // proxy minima per quarter of the block (A/B: DESIGN.md 9b)
+#endif
+            constexpr uint32_t NQ = HRB_P3_Q, QL = BLK / NQ;
+            uint32_t lq[NQ];
+#pragma unroll
+            for (uint32_t q = 0; q < NQ; q++) lq[q] = 0xFFFFFFFFu;
             // two arguments per iteration, four instructions: t = u(x+1);
             // a three-input min; u(x+2) = t + d + e as one three-input add
             // (IADD3 -- an ALU-pipe op; two-input adds alone all went to the
@@ -669,19 +675,22 @@ __global__ void __launch_bounds__(256, HRB_P3_MINB) phase3_kernel(SliceDev s, in
                 // the same values, keeps them in local memory for it
                 uint32_t t;
                 asm("add.u32 %0, %1, %2;" : "=r"(t) : "r"(u), "r"(d));
-                lo_top = min(lo_top, min(u, t));
+                lq[x / QL] = min(lq[x / QL], min(u, t));
                 asm("{\n\t.reg .u32 w;\n\tadd.u32 w, %1, %2;\n\tadd.u32 %0, w, %3;\n\t}"
                     : "=r"(u) : "r"(t), "r"(d), "r"(e32));
                 asm("add.u32 %0, %0, %1;" : "+r"(d) : "r"(e2x32));
 #else
                 const uint32_t t = u + d;
-                lo_top = min(lo_top, min(u, t));
+                lq[x / QL] = min(lq[x / QL], min(u, t));
                 u = t + d + e32;
                 d += e2x32;
 #endif
             }
             V += (D1 << LBLK) + D2xCB;  // exact: BLK steps of V += D1, D1 += D2
             D1 += D2xB;
+            uint32_t lo_top = lq[0];
+#pragma unroll
+            for (uint32_t q = 1; q < NQ; q++) lo_top = min(lo_top, lq[q]);
             const bool any = x0 < len && lo_top <= KtopM;
             if (__any_sync(0xffffffffu, any)) {
                 // rare: replay the proxy over the block into a per-lane mask
@@ -692,13 +701,28 @@ __global__ void __launch_bounds__(256, HRB_P3_MINB) phase3_kernel(SliceDev s, in
                 // lane appends its hits in argument order
                 Mask fl = 0;
                 if (any) {
-                    uint32_t pu = (uint32_t)(V0 >> 96) + MARGIN, pd = (uint32_t)(D10 >> 96);
+                    // only the quarters whose proxy minimum flagged; the proxy
+                    // at a quarter's start in closed form (mod 2^32, the same
+                    // values the walk stepped through)
+                    const uint32_t u0 = (uint32_t)(V0 >> 96) + MARGIN, d0 = (uint32_t)(D10 >> 96);
 #pragma unroll
-                    for (uint32_t x = 0; x < BLK; x++) {
-                        fl |= (x0 + x < len && pu <= KtopM) ? ((Mask)1 << x) : (Mask)0;
-                        pu += pd;
-                        pd += e32;
+                    for (uint32_t q = 0; q < NQ; q++) {
+                        if (lq[q] <= KtopM) {
+                            const uint32_t xq = q * QL;
+                            uint32_t pu = u0 + xq * d0 + ((xq * (xq - 1)) >> 1) * e32, pd = d0 + xq * e32;
+                            using QMask = typename std::conditional<(QL > 32), Mask, uint32_t>::type;
+                            QMask m = 0;
+#pragma unroll
+                            for (uint32_t x = 0; x < QL; x++) {
+                                m |= pu <= KtopM ? ((QMask)1 << x) : (QMask)0;
+                                pu += pd;
+                                pd += e32;
+                            }
+                            fl |= (Mask)m << xq;
+                        }
                     }
+                    const uint32_t lim = len - x0;  // > 0 here
+                    if (lim < BLK) fl &= ((Mask)1 << lim) - 1;
                 }
                 while (__any_sync(0xffffffffu, fl != 0)) {
                     bool hit = false;
